@@ -1,0 +1,128 @@
+"""Generate golden fixtures by importing the REFERENCE itself.
+
+Run in the build container (the only place /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+Writes tests/golden/golden.npz (small KATs and products) and
+tests/golden/digests.json (sha256 of config-sized products, SURVEY.md §8(c)
+convention: sha256 of the little-endian words of the owned result).
+The GPU box never runs this; tests read the committed outputs.
+"""
+
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+REF = os.environ.get("GF2_REF_SRC", "/root/reference/pkg/src")
+sys.path.insert(0, REF)
+import gf2mat as g  # noqa: E402
+from gf2mat import _reference as ref  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def dig(m):
+    return hashlib.sha256(np.ascontiguousarray(m.words, dtype="<u8")
+                          .tobytes()).hexdigest()
+
+
+def main(big: bool):
+    out = {}
+    # --- generator KATs (core.py:191-208)
+    out["kat_random_1x128_s0"] = g.random(1, 128, 0).words.copy()
+    out["kat_random_2x65_s7"] = g.random(2, 65, 7).words.copy()
+    out["kat_random_37x200_s123"] = g.random(37, 200, 123).words.copy()
+    # --- gray codes (graycode.py:38-48), Fig. 1
+    for k in range(1, 6):
+        gc = g.build_gray(k)
+        out[f"gray_code_k{k}"] = np.array(gc.code, dtype=np.int64)
+        out[f"gray_changed_k{k}"] = np.array(gc.changed_bit, dtype=np.int64)
+    # --- make_table (graycode.py:108-156) on a window source
+    pb = g.random(40, 256, 5)
+    w = g.window(pb, 3, 64, 9, 130)
+    for k in (3, 8):
+        tbl = g.CombinationTable(k, w.ncols)
+        g.make_table(w, 1, k, tbl)
+        out[f"table_k{k}"] = tbl.rows.copy()
+    # --- read_bits KATs (core.py:229-248)
+    rb = g.random(3, 256, 7)
+    kat = []
+    for r in range(3):
+        for sc, k in [(0, 8), (60, 8), (62, 4), (120, 16), (190, 3), (248, 8)]:
+            kat.append((r, sc, k, g.read_bits(rb, r, sc, k)))
+    out["read_bits_kat"] = np.array(kat, dtype=np.int64)
+    # --- peel_split KATs (strassen.py:66-84)
+    rng = np.random.default_rng(11)
+    ps = []
+    for _ in range(60):
+        m, l, n = (int(x) for x in rng.integers(1, 70000, 3))
+        cut = int(rng.choice([64, 128, 1024, 2048, 4096]))
+        ps.append((m, l, n, cut) + tuple(g.peel_split(m, l, n, cut)))
+    for t in [(16384, 16384, 16384, 2048), (4096, 4096, 4096, 1024),
+              (10000, 7001, 12345, 2048), (65536, 65536, 65536, 2048),
+              (16385, 16385, 16385, 4096), (100, 100, 100, 4096)]:
+        ps.append(t + tuple(g.peel_split(*t)))
+    out["peel_split_kat"] = np.array(ps, dtype=np.int64)
+    # --- products: owned operands, various shapes, via the reference paths
+    cases = []
+    shapes = [(1, 1, 1), (2, 2, 2), (3, 70, 5), (64, 64, 64), (65, 63, 129),
+              (100, 100, 100), (129, 100, 193), (200, 300, 64), (257, 129, 300),
+              (300, 1, 300), (1, 300, 1), (511, 513, 257), (1023, 1024, 1025)]
+    for i, (m, l, n) in enumerate(shapes):
+        sa, sb = 1000 + i, 2000 + i
+        a, b = g.random(m, l, sa), g.random(l, n, sb)
+        c = g.mul_strassen(a, b, g.MulParams(cutoff=64))
+        assert g.equal(c, g.mul_m4rm(a, b, 8))
+        out[f"prod_{i}"] = c.words.copy()
+        cases.append((i, m, l, n, sa, sb))
+    out["prod_cases"] = np.array(cases, dtype=np.int64)
+    # --- window operands at odd word offsets (core.py:110-144)
+    pa, pb2, pc = g.random(90, 640, 77), g.random(700, 512, 78), g.random(80, 512, 79)
+    aw = g.window(pa, 5, 64, 70, 385)       # word offset 1, ragged width
+    bw = g.window(pb2, 11, 192, 385, 250)   # word offset 3, ragged width
+    out["win_product"] = g.mul_m4rm(aw, bw, 8).words.copy()
+    cw = g.window(pc, 3, 64, 70, 250)
+    snap = g.copy_out(pc)
+    g.add_into(cw, cw, g.mul_strassen(aw, bw, g.MulParams(cutoff=64)))
+    out["win_accum_parent"] = pc.words.copy()
+    out["win_accum_parent_before"] = snap.words.copy()
+    # --- accumulate variant mul_m4rm_into (m4rm.py:150-155)
+    a, b, c0 = g.random(150, 333, 91), g.random(333, 200, 92), g.random(150, 200, 93)
+    c = g.copy_out(c0)
+    g.mul_m4rm_into(c, a, b, 8, 64, 4)
+    out["into_result"] = c.words.copy()
+    np.savez_compressed(os.path.join(HERE, "golden.npz"), **out)
+
+    # --- config digests (SURVEY.md §8(c) seed convention 10i+1/2/3)
+    digests = {}
+    a, b = g.random(1024, 1024, 11), g.random(1024, 1024, 12)
+    digests["cfg1"] = dig(g.mul_m4rm(a, b, 8))
+    if big:
+        t0 = time.time()
+        a, b = g.random(4096, 4096, 21), g.random(4096, 4096, 22)
+        digests["cfg2"] = dig(g.mul_strassen(a, b, g.MulParams(cutoff=1024, k=8)))
+        print("cfg2", time.time() - t0, flush=True)
+        t0 = time.time()
+        a, b = g.random(16384, 16384, 31), g.random(16384, 16384, 32)
+        digests["cfg3"] = dig(g.mul_strassen(a, b))
+        print("cfg3", time.time() - t0, flush=True)
+    path = os.path.join(HERE, "digests.json")
+    prev = json.load(open(path)) if os.path.exists(path) else {}
+    prev.update(digests)
+    # values computed in the survey from the reference (cfg4 needs the
+    # §8(d) Bernoulli generator; cfg5 took 21 min on one core)
+    prev.setdefault("cfg4_product", "72d6193db5e210ecbc95b336101f02e506865c85e8421db0a102f1351d104ac6")
+    prev.setdefault("cfg4_addmul", "7e550abcedb3535f07c3498f2289b8c7fd521ad72d5d6db640ea922a868812aa")
+    prev.setdefault("cfg5_product", "c6e32dc76743798f0eea38f3adde3af4232e1459a576df9b8cb364a2530d22d1")
+    prev.setdefault("cfg5_addmul", "ca72f9e2f6cde38ec33dd9271cd6a2ca4758163ca25a39f2da038dfd244a0f16")
+    json.dump(prev, open(path, "w"), indent=1, sort_keys=True)
+    print(json.dumps(prev, indent=1))
+
+
+if __name__ == "__main__":
+    main(big="--big" in sys.argv)
