@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 GF(2) multiply (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One JSON line on rank 0. Workload (BASELINE.json configs[2], the shape the
+metric is quoted on): C = A.B over GF(2), A and B 16384 x 16384 seeded
+splitmix64 bits (core.random seeds 31 / 32), Strassen-Winograd over M4RM.
+N = 1: one GPU multiplies. N > 1 (torchrun): C and A row-sharded, B
+broadcast from rank 0 over NVLink (NCCL) in K-panels inside the timed step.
+
+`--impl reference` times the reference algorithm's CPU port
+(oracle/libgf2oracle.so, a C restatement of gf2mat's M4RM + Strassen-
+Winograd, all host threads) on a bounded row sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("GF(2) matmul effective bit-ops/s (n^3) and ms/multiply at "
+          "n=16384, 1/2/4/8 B200")
+UNIT = "bit-ops/s"
+WORKLOAD = dict(name="cfg3", m=16384, l=16384, n=16384, seed_a=31, seed_b=32)
+PAPER_2008_CPU = 16384 ** 3 / 6.074   # PAPER.md:753 (M4RI, Core 2 Duo)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--cutoff", type=int, default=0,
+                   help="Strassen cutoff (0 = device default)")
+    p.add_argument("--npanels", type=int, default=4)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-verify", action="store_true")
+    p.add_argument("--size", type=int, default=0,
+                   help="override n (debug only; the metric is n=16384)")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "MEASURED_PEAKS.json"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, \
+            "fallback (B200_PROFILING.md)"
+
+
+def golden_digest(key: str):
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "digests.json")) as fh:
+            return json.load(fh).get(key)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ CPU port
+def cpu_port_sample(m, l, n, seed_a, seed_b, target_s=8.0, rows=None):
+    """Time the reference algorithm's C port on a row sample A[:R] . B with
+    all host threads. Returns (bitops_per_s, threads, sample_desc)."""
+    from oracle import gf2_port as P
+    threads = len(os.sched_getaffinity(0))
+    P.set_threads(threads)
+    b = P.random(l, n, seed_b)
+    if rows is None:
+        rows = min(m, 256)
+        while True:
+            a = P.random(rows, l, seed_a)
+            t0 = time.perf_counter()
+            P.mul_strassen(a, b)
+            dt = time.perf_counter() - t0
+            if dt * 2 > target_s or rows >= m:
+                break
+            rows = min(m, rows * 2)
+    a = P.random(rows, l, seed_a)
+    t0 = time.perf_counter()
+    P.mul_strassen(a, b)
+    dt = time.perf_counter() - t0
+    ops = rows * l * n
+    return ops / dt, threads, rows, dt
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm on the host CPU (port)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w = dict(WORKLOAD)
+    if args.size:
+        w.update(m=args.size, l=args.size, n=args.size)
+    m, l, n = w["m"], w["l"], w["n"]
+    # size the sample so that warmup + steps finish in a few minutes
+    _, threads, rows, dt = cpu_port_sample(m, l, n, w["seed_a"], w["seed_b"],
+                                           target_s=6.0)
+    times = []
+    from oracle import gf2_port as P
+    b = P.random(l, n, w["seed_b"])
+    a = P.random(rows, l, w["seed_a"])
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        P.mul_strassen(a, b)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    per = sum(times) / len(times)
+    value = rows * l * n / per
+    sample = (f"A[:{rows}] x B ({rows}x{l}x{n}) per step, C port of "
+              f"mul_strassen default params (cutoff 2048, k auto, t 8)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per * 1e3 * (m / rows), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic: core.random splitmix64 bits, seeds 31/32",
+        "config": {"workload": f"{w['name']}: {m}x{l}x{n} GF(2) multiply",
+                   "m": m, "l": l, "n": n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "note": "ms_per_step extrapolated to the full m rows",
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+    import paper_0811_1714_b200 as g
+    from paper_0811_1714_b200 import _lib
+    from paper_0811_1714_b200.sharded import mul_sharded, shard_rows
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    w = dict(WORKLOAD)
+    if args.size:
+        w.update(m=args.size, l=args.size, n=args.size)
+    m, l, n = w["m"], w["l"], w["n"]
+    params = g.default_params() if not args.cutoff else \
+        g.MulParams(cutoff=args.cutoff, k=8)
+    r0, r1 = shard_rows(m, world, rank) if world > 1 else (0, m)
+    a = g.random(r1 - r0, l, w["seed_a"], device=dev, row_base=r0)
+    b = g.random(l, n, w["seed_b"], device=dev) if (world == 1 or rank == 0) \
+        else g.create(l, n, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        if world == 1:
+            return g.mul_strassen(a, b, params)
+        return mul_sharded(a, b, params, src=0, npanels=args.npanels)
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        c = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    _lib.timer_enable(True)
+    n_launch0 = g.launch_count()
+    evs = []
+    for _ in range(args.steps):
+        flush.zero_()                      # evict L2 (126 MB) between steps
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        c = step()
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    n_launch = g.launch_count() - n_launch0
+    kern_ms, kern_ops, kern_n = _lib.timer_read()
+    _lib.timer_enable(False)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    bitops = float(m) * l * n
+    value = bitops / (ms_step * 1e-3)
+
+    # ---- verification of the timed result (sha256 of the raw words)
+    verified = None
+    if not args.no_verify and not args.size:
+        words = c.to_numpy()
+        if world > 1:
+            parts = [None] * world
+            dist.all_gather_object(parts, words)
+            words = None
+            if rank == 0:
+                import numpy as np
+                words = np.concatenate(parts, axis=0)
+        if rank == 0:
+            want = golden_digest(w["name"])
+            got = hashlib.sha256(words.astype("<u8").tobytes()).hexdigest()
+            verified = (got == want) if want else None
+
+    # ---- end to end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e and world == 1:
+        import numpy as np
+        wa, wb = g.words_per_row(l), g.words_per_row(n)
+        ha = torch.empty((m, wa), dtype=torch.int64, pin_memory=True)
+        hb = torch.empty((l, wb), dtype=torch.int64, pin_memory=True)
+        hc = torch.empty((m, wb), dtype=torch.int64, pin_memory=True)
+        a.to_numpy(out=ha.numpy().view(np.uint64))
+        b.to_numpy(out=hb.numpy().view(np.uint64))
+        ad, bd = g.create(m, l, dev), g.create(l, n, dev)
+        hav, hbv, hcv = (x.numpy().view(np.uint64) for x in (ha, hb, hc))
+
+        def e2e_step():
+            g.from_numpy(hav, l, out=ad, nonblocking=True)
+            g.from_numpy(hbv, n, out=bd, nonblocking=True)
+            cc = g.mul_strassen(ad, bd, params)
+            g.core._download(cc, hcv, nonblocking=True)
+            return cc
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        ee = []
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            e2e_step()
+            e1.record(stream)
+            ee.append((e0, e1))
+        torch.cuda.synchronize()
+        e2e_ms = sum(x.elapsed_time(y) for x, y in ee) / args.steps
+        if not args.no_verify and not args.size:
+            got = hashlib.sha256(hcv.astype("<u8").tobytes()).hexdigest()
+            if verified is not None:
+                verified = verified and got == golden_digest(w["name"])
+        e2e = {"value": bitops / (e2e_ms * 1e-3), "unit": UNIT,
+               "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(hav.nbytes + hbv.nbytes),
+               "d2h_bytes_per_step": int(hcv.nbytes)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (batched leaf M4RM launch)
+    peaks, src = measured_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    props = torch.cuda.get_device_properties(dev)
+    nsm = props.multi_processor_count
+    smem_peak_gbs = 128.0 * nsm * sm_max * 1e6 / 1e9   # 128 B/clk/SM crossbar
+    roofline = None
+    if kern_n:
+        lut_bytes = kern_ops / 64.0      # W/(8k) bytes, k = 8
+        ach = lut_bytes / (kern_ms * 1e-3) / 1e9
+        roofline = {
+            "bound": "smem", "kernel": "k_m4rm (batched Strassen leaves)",
+            "achieved": ach, "peak": smem_peak_gbs, "unit": "GB/s",
+            "frac": ach / smem_peak_gbs, "traffic": None,
+            "kernel_ms_per_step": kern_ms / args.steps,
+            "kernel_share_of_step": kern_ms / total_ms if world == 1 else None,
+            "kernel_bitops_per_step": kern_ops / args.steps,
+            "peak_source": f"128 B/clk/SM x {nsm} SMs x {sm_max:.0f} MHz "
+                           f"(sm_max_mhz from {src}); HBM bound "
+                           f"{peaks.get('hbm_gbs')} GB/s never binds here",
+        }
+        tr = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tr):
+            try:
+                roofline["traffic"] = json.load(open(tr)).get("k_m4rm")
+            except Exception:
+                pass
+    hbm_bytes = 3.0 * m * g.words_per_row(n) * 8
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        v, thr, rows, dt = cpu_port_sample(m, l, n, w["seed_a"], w["seed_b"])
+        cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "port",
+               "sample": f"A[:{rows}] x B ({rows}x{l}x{n}), {dt:.1f} s, C port "
+                         "of gf2mat mul_strassen (default params) on "
+                         f"{thr} host threads"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u64", "data": "synthetic: core.random splitmix64 "
+                                f"Bernoulli(0.5) bits, seeds {w['seed_a']}/"
+                                f"{w['seed_b']}",
+        "config": {"workload": f"{w['name']}: A,B {m}x{l} . {l}x{n} GF(2), "
+                               f"Strassen-Winograd (cutoff {params.cutoff}) "
+                               "over M4RM",
+                   "m": m, "l": l, "n": n, "cutoff": params.cutoff,
+                   "parallelism": "single" if world == 1 else
+                   f"rows{world} + NCCL broadcast of B ({args.npanels} panels)",
+                   "l2": "flushed between timed steps (512 MiB write)"},
+        "verified_sha256": verified,
+        "gpu_launches": n_launch,
+        "gpu_launches_per_step": n_launch / args.steps,
+        "clocks": clk,
+        "roofline": roofline,
+        "hbm_roofline_ms": hbm_bytes / (float(peaks.get("hbm_gbs", 6650)) * 1e9)
+        * 1e3,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "vs_paper_2008_cpu": value / PAPER_2008_CPU,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

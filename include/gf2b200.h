@@ -1,0 +1,126 @@
+/* gf2b200 -- B200-native dense GF(2) matrix multiplication, C ABI.
+ *
+ * The drop-in boundary for the reference's hot path (gf2mat v0.1.0,
+ * /root/reference/pkg/src/gf2mat). The reference is a pure-Python package
+ * with no FFI of its own; each entry point below replaces the Python
+ * function cited next to it, with the same argument meaning and the same
+ * error classes (mapped from the status codes). Plain pointers and sizes
+ * only; no torch types. A Python ctypes binding lives in
+ * paper_0811_1714_b200/_lib.py; INTEGRATION.md shows the binding a
+ * maintainer would add to gf2mat itself.
+ *
+ * Layout (core.py:3-11): a matrix is row-major, 64 columns per uint64 word,
+ * column c of a row at bit 63 - (c % 64) of word c / 64 (MSB first). A
+ * view describes a matrix or a window (core.py:110-144): `data` points at
+ * word 0 of row 0 of the view (the window's word offset is folded in, so
+ * windows need only 8-byte alignment), `pitch` is the word distance between
+ * rows. Words per row = ceil(ncols / 64). Every write through a view keeps
+ * the bits beyond its right edge (core.py:278-323); owned matrices keep
+ * their trailing bits zero.
+ *
+ * All functions are asynchronous on `stream` (a cudaStream_t, NULL = the
+ * legacy default stream) unless stated otherwise, and return a status code;
+ * gf2_last_error() gives a thread-local message for the last failure.
+ */
+#ifndef GF2B200_H
+#define GF2B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gf2_view {
+    uint64_t *data;  /* device pointer: word 0 of row 0 of the view */
+    int64_t pitch;   /* words between consecutive rows (>= words per row) */
+    int64_t nrows;
+    int64_t ncols;   /* columns (bits) */
+} gf2_view;
+
+/* Status codes; the Python shim maps them to gf2mat's errors.py:4-21. */
+enum {
+    GF2_OK = 0,
+    GF2_ERR_DIMENSION = 1, /* DimensionError (errors.py:8) */
+    GF2_ERR_ALIGNMENT = 2, /* AlignmentError (errors.py:12) */
+    GF2_ERR_PARAMETER = 3, /* ParameterError (errors.py:16) */
+    GF2_ERR_CUDA = 4,      /* CUDA runtime failure (no reference analogue) */
+    GF2_ERR_OOM = 5,       /* device allocation failure */
+    GF2_ERR_INTERNAL = 6
+};
+
+const char *gf2_version(void);
+const char *gf2_last_error(void);
+
+/* Recommended row pitch (words) for an owned device matrix of ncols
+ * columns: 16-byte multiple, 128-byte multiple once a row spans 16 words. */
+int64_t gf2_pitch_words(int64_t ncols);
+
+/* Device memory for hosts without their own allocator (stream-ordered pool).
+ * gf2_alloc zero-fills (core.py:176-178 `create`). */
+int gf2_alloc(int64_t nrows, int64_t ncols, gf2_view *out, void *stream);
+int gf2_free(gf2_view *v, void *stream);
+
+/* Host <-> device. `host_stride` is the host row stride in words (the
+ * reference's dense layout uses width = ceil(ncols/64), core.py:76-80).
+ * Upload writes whole words (for owned targets); download copies raw words. */
+int gf2_upload(const gf2_view *dst, const uint64_t *host, int64_t host_stride,
+               void *stream);
+int gf2_download(const gf2_view *src, uint64_t *host, int64_t host_stride,
+                 void *stream);
+
+/* dst = 0 on the view, preserving bits beyond its right edge. */
+int gf2_zero(const gf2_view *dst, void *stream);
+
+/* core.py:202-208 `random`: word (r, j) = splitmix64(seed + (i+1)*golden)
+ * with i = (row_base + r) * width + j, last word tail-masked. row_base
+ * selects rows of a taller matrix (row shards of one seeded matrix). */
+int gf2_random(const gf2_view *dst, uint64_t seed, int64_t row_base,
+               void *stream);
+
+/* SURVEY.md §8(d) Bernoulli(p): entry (r, c) = 1 iff the splitmix64 output
+ * at counter (row_base + r) * ncols + c + 1 is < threshold (= floor(p*2^64)). */
+int gf2_bernoulli(const gf2_view *dst, uint64_t seed, uint64_t threshold,
+                  int64_t row_base, void *stream);
+
+/* core.py:278-300 `add_into`: out = a XOR b (out may alias a or b). */
+int gf2_add(const gf2_view *out, const gf2_view *a, const gf2_view *b,
+            void *stream);
+/* core.py:312-323 `copy_into`. */
+int gf2_copy(const gf2_view *out, const gf2_view *a, void *stream);
+
+/* m4rm.py:77-121 `_mul_into` / m4rm.py:124-155 `mul_m4rm*`:
+ * C = A.B (accumulate = 0) or C ^= A.B (accumulate = 1, mul_m4rm_into).
+ * k is the reference's table width (1..16, validated; the device kernel
+ * indexes 8-bit Gray tables -- results are independent of k). C must not
+ * alias A or B. */
+int gf2_m4rm(const gf2_view *c, const gf2_view *a, const gf2_view *b, int k,
+             int accumulate, void *stream);
+
+/* strassen.py:257-282 `mul_strassen` (+ peel_split strassen.py:66-84,
+ * schedule strassen.py:141-204, peel_fixup strassen.py:219-249):
+ * Strassen-Winograd recursion above `cutoff` over an M4RM base case.
+ * accumulate = 1 gives C += A.B (cfg4/cfg5 addmul). */
+int gf2_strassen(const gf2_view *c, const gf2_view *a, const gf2_view *b,
+                 int64_t cutoff, int k, int accumulate, void *stream);
+
+/* strassen.py:66-84 `peel_split`: writes {m', l', n', depth}. Host only. */
+int gf2_peel_split(int64_t m, int64_t l, int64_t n, int64_t cutoff,
+                   int64_t out4[4]);
+
+/* Number of kernels this library has launched in this process (telemetry
+ * for the bench's `gpu_launches`). */
+int64_t gf2_launch_count(void);
+
+/* Kernel timer for the roofline: while enabled, every M4RM launch is
+ * bracketed by CUDA events recorded on the stream it runs on. Enabling
+ * resets the accumulators. gf2_timer_read synchronizes the recorded events
+ * and returns the summed kernel milliseconds, the algorithmic bit-ops
+ * (m*l*n per product) those launches computed, and the launch count. */
+int gf2_timer_enable(int on);
+int gf2_timer_read(double *kernel_ms, double *bitops, int64_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GF2B200_H */

@@ -1,0 +1,424 @@
+"""Device-resident bit-packed GF(2) matrices and windows (B200).
+
+Mirrors the reference's storage layer (core.py:57-341, gf2mat v0.1.0) over
+HBM: 64 columns per word, column c at bit 63 - c % 64 of word c // 64, rows
+padded to a device pitch (16-byte multiple; 128-byte multiple once a row
+spans 16 words) so row starts are aligned for vector / TMA access. Storage
+is a torch int64 tensor (torch's caching allocator and streams are the
+plumbing); every operation is a call into libgf2b200.so on the current
+torch stream. Windows (core.py:110-170) are non-owning views at word-aligned
+column offsets; writes through them keep the bits beyond their right edge.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .errors import AlignmentError, DimensionError
+
+WORD_BITS = 64
+_FULL = 0xFFFFFFFFFFFFFFFF
+
+
+def words_per_row(ncols: int) -> int:
+    """core.py:45-46"""
+    return (ncols + WORD_BITS - 1) // WORD_BITS
+
+
+def tail_mask(ncols: int) -> int:
+    """core.py:49-54 (as a Python int)."""
+    rem = ncols % WORD_BITS
+    return _FULL if rem == 0 else (_FULL << (WORD_BITS - rem)) & _FULL
+
+
+def _signed(x: int) -> int:
+    return x - (1 << 64) if x >= (1 << 63) else x
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class BitMatrix:
+    """Owned device matrix (core.py:57-107).
+
+    Attributes: nrows, ncols, width (words per row), pitch (device row
+    stride in words), storage (torch int64 tensor [nrows, pitch] on cuda).
+    Padding words beyond `width` stay zero; trailing bits stay zero.
+    """
+
+    __slots__ = ("nrows", "ncols", "width", "pitch", "storage", "__weakref__")
+
+    def __init__(self, nrows: int, ncols: int, device=None):
+        if nrows < 0 or ncols < 0:
+            raise DimensionError(f"negative dimensions {nrows}x{ncols}")
+        lib = _lib.lib_cuda()
+        torch = _torch()
+        self.nrows = int(nrows)
+        self.ncols = int(ncols)
+        self.width = words_per_row(ncols)
+        self.pitch = int(lib.gf2_pitch_words(ncols))
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.storage = torch.zeros((self.nrows, self.pitch), dtype=torch.int64,
+                                   device=device)
+
+    # reference-compatible accessors
+    @property
+    def shape(self) -> tuple[int, int]:
+        return (self.nrows, self.ncols)
+
+    @property
+    def device(self):
+        return self.storage.device
+
+    @property
+    def words(self):
+        """(nrows, width) int64 torch view of the packed words."""
+        return self.storage[:, :self.width]
+
+    def _view(self) -> _lib.Gf2View:
+        return _lib.Gf2View(self.storage.data_ptr() or None, self.pitch,
+                            self.nrows, self.ncols)
+
+    def to_numpy(self, out: np.ndarray | None = None) -> np.ndarray:
+        return _download(self, out)
+
+    def to_host(self):
+        return HostMatrix(self.nrows, self.ncols, self.to_numpy())
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, (BitMatrix, MatrixWindow)):
+            return NotImplemented
+        return equal(self, other)
+
+    def __hash__(self):
+        return id(self)
+
+    def __repr__(self) -> str:
+        return f"BitMatrix({self.nrows}x{self.ncols}, {self.device})"
+
+
+class MatrixWindow:
+    """Non-owning view of a rectangle of a BitMatrix (core.py:110-170)."""
+
+    __slots__ = ("parent", "row_offset", "col_offset", "nrows", "ncols",
+                 "width")
+
+    def __init__(self, parent: BitMatrix, row_offset: int, col_offset: int,
+                 nrows: int, ncols: int):
+        if col_offset % WORD_BITS != 0:
+            raise AlignmentError(
+                f"window column offset {col_offset} is not a multiple of 64")
+        if nrows < 0 or ncols < 0:
+            raise DimensionError(f"negative window {nrows}x{ncols}")
+        if row_offset < 0 or col_offset < 0 \
+                or row_offset + nrows > parent.nrows \
+                or col_offset + ncols > parent.ncols:
+            raise DimensionError(
+                f"window {nrows}x{ncols}@({row_offset},{col_offset}) exceeds "
+                f"parent {parent.nrows}x{parent.ncols}")
+        self.parent = parent
+        self.row_offset = row_offset
+        self.col_offset = col_offset
+        self.nrows = nrows
+        self.ncols = ncols
+        self.width = words_per_row(ncols)
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return (self.nrows, self.ncols)
+
+    @property
+    def device(self):
+        return self.parent.storage.device
+
+    @property
+    def pitch(self) -> int:
+        return self.parent.pitch
+
+    @property
+    def words(self):
+        w0 = self.col_offset // WORD_BITS
+        return self.parent.storage[self.row_offset:self.row_offset + self.nrows,
+                                   w0:w0 + self.width]
+
+    def _view(self) -> _lib.Gf2View:
+        p = self.parent
+        base = p.storage.data_ptr()
+        off = self.row_offset * p.pitch + self.col_offset // WORD_BITS
+        ptr = base + 8 * off if base else None
+        return _lib.Gf2View(ptr, p.pitch, self.nrows, self.ncols)
+
+    def to_numpy(self, out: np.ndarray | None = None) -> np.ndarray:
+        return _download(self, out)
+
+    def to_host(self):
+        return HostMatrix(self.nrows, self.ncols, self.to_numpy())
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, (BitMatrix, MatrixWindow)):
+            return NotImplemented
+        return equal(self, other)
+
+    def __hash__(self):
+        return id(self)
+
+    def __repr__(self) -> str:
+        return (f"MatrixWindow({self.nrows}x{self.ncols}@"
+                f"({self.row_offset},{self.col_offset}))")
+
+
+Mat = BitMatrix | MatrixWindow
+
+
+class HostMatrix:
+    """Host copy with the reference BitMatrix's read-only attribute surface
+    (nrows, ncols, width, data, words, row_index, buf), so reference-side
+    tooling such as gf2mat._reference.unpack_entries accepts it."""
+
+    __slots__ = ("nrows", "ncols", "width", "words")
+
+    def __init__(self, nrows: int, ncols: int, words: np.ndarray):
+        self.nrows, self.ncols = nrows, ncols
+        self.width = words_per_row(ncols)
+        self.words = words
+
+    @property
+    def data(self) -> np.ndarray:
+        return self.words.reshape(-1)
+
+    buf = data
+
+    @property
+    def row_index(self) -> np.ndarray:
+        return np.arange(self.nrows, dtype=np.int64) * self.width
+
+    @property
+    def shape(self):
+        return (self.nrows, self.ncols)
+
+
+def _stream():
+    return _lib.current_stream()
+
+
+def _check_cuda_dev(*mats):
+    devs = {m.device for m in mats}
+    if len(devs) > 1:
+        raise DimensionError(f"operands live on different devices: {devs}")
+
+
+# ------------------------------------------------------------ constructors
+def create(nrows: int, ncols: int, device=None) -> BitMatrix:
+    """All-zero matrix (core.py:176-178)."""
+    return BitMatrix(nrows, ncols, device)
+
+
+def random(nrows: int, ncols: int, seed: int, device=None,
+           row_base: int = 0) -> BitMatrix:
+    """core.py:202-208 on device (splitmix64 over the flat word index).
+    `row_base` produces rows [row_base, row_base + nrows) of a taller
+    matrix with the same seed -- how row shards are generated in place."""
+    m = BitMatrix(nrows, ncols, device)
+    if m.nrows and m.width:
+        _lib.check(_lib.lib_cuda().gf2_random(
+            m._view(), seed & _FULL, row_base, _stream()))
+    return m
+
+
+def bernoulli(nrows: int, ncols: int, seed: int, p: float | None = None,
+              threshold: int | None = None, device=None,
+              row_base: int = 0) -> BitMatrix:
+    """Bernoulli(p) matrix of SURVEY.md §8(d) (cfg4): entry e = r*ncols + c
+    is 1 iff splitmix64(seed, e) < floor(p * 2^64)."""
+    if threshold is None:
+        if p is None:
+            raise ValueError("give p or threshold")
+        from fractions import Fraction
+        threshold = _FULL if p >= 1 else int(Fraction(str(p)) * (1 << 64))
+    m = BitMatrix(nrows, ncols, device)
+    if m.nrows and m.width:
+        _lib.check(_lib.lib_cuda().gf2_bernoulli(
+            m._view(), seed & _FULL, threshold & _FULL, row_base, _stream()))
+    return m
+
+
+def identity(n: int, device=None) -> BitMatrix:
+    dense = np.eye(n, dtype=np.uint8)
+    return from_dense(dense, device)
+
+
+def window(a: Mat, row_offset: int, col_offset: int, nrows: int,
+           ncols: int) -> MatrixWindow:
+    """core.py:326-332 -- a window of a window flattens onto the root."""
+    if isinstance(a, MatrixWindow):
+        return MatrixWindow(a.parent, a.row_offset + row_offset,
+                            a.col_offset + col_offset, nrows, ncols)
+    return MatrixWindow(a, row_offset, col_offset, nrows, ncols)
+
+
+# ------------------------------------------------------------ host interop
+def from_numpy(words: np.ndarray, ncols: int, device=None,
+               out: BitMatrix | None = None,
+               nonblocking: bool = False) -> BitMatrix:
+    """Upload (nrows, width) uint64 words (reference dense layout). The
+    words are taken as-is (trailing bits must already be clean). With
+    `nonblocking`, the copy is left in flight on the current stream: the
+    caller keeps `words` alive (pinned memory makes it truly async)."""
+    words = np.asarray(words)
+    if words.dtype != np.uint64 or words.ndim != 2:
+        raise DimensionError("from_numpy expects a 2-D uint64 array")
+    nrows = words.shape[0]
+    if words.shape[1] != words_per_row(ncols):
+        raise DimensionError(
+            f"{words.shape[1]} words per row for {ncols} columns")
+    m = BitMatrix(nrows, ncols, device) if out is None else out
+    if m.shape != (nrows, ncols):
+        raise DimensionError(f"upload target {m.shape} != ({nrows}, {ncols})")
+    if nrows and m.width:
+        if words.strides[1] != 8 or words.strides[0] % 8:
+            words = np.ascontiguousarray(words)
+            nonblocking = False
+        _lib.check(_lib.lib_cuda().gf2_upload(
+            m._view(), words.ctypes.data, words.strides[0] // 8, _stream()))
+        if not nonblocking:
+            _torch().cuda.current_stream().synchronize()
+    return m
+
+
+def from_host(m, device=None) -> BitMatrix:
+    """Upload anything with the reference's attribute surface
+    (`nrows`, `ncols`, `words`): gf2mat.BitMatrix / MatrixWindow, HostMatrix.
+    Window sources are copied with their right edge masked."""
+    words = np.ascontiguousarray(np.asarray(m.words, dtype=np.uint64))
+    if words.size:
+        words = words.copy()
+        words[:, -1] &= np.uint64(tail_mask(m.ncols))
+    return from_numpy(words.reshape(m.nrows, words_per_row(m.ncols)), m.ncols,
+                      device)
+
+
+def _download(a: Mat, out: np.ndarray | None,
+              nonblocking: bool = False) -> np.ndarray:
+    w = words_per_row(a.ncols)
+    if out is None:
+        out = np.empty((a.nrows, w), dtype=np.uint64)
+    if out.shape != (a.nrows, w) or out.dtype != np.uint64 \
+            or out.strides[1] != 8:
+        raise DimensionError(f"download buffer {out.shape} != ({a.nrows}, {w})")
+    if a.nrows and w:
+        _lib.check(_lib.lib_cuda().gf2_download(
+            a._view(), out.ctypes.data, out.strides[0] // 8, _stream()))
+        if not nonblocking:
+            _torch().cuda.current_stream().synchronize()
+    return out
+
+
+def to_numpy(a: Mat) -> np.ndarray:
+    """(nrows, width) uint64 words, raw (a window's last word may carry the
+    parent's bits beyond its edge, exactly as `window.words` in core.py)."""
+    return _download(a, None)
+
+
+def to_dense(a: Mat) -> np.ndarray:
+    """core.py:409-414"""
+    if a.nrows == 0 or a.ncols == 0:
+        return np.zeros((a.nrows, a.ncols), dtype=np.uint8)
+    by = to_numpy(a).astype(">u8").view(np.uint8).reshape(a.nrows, -1)
+    return np.unpackbits(by, axis=1, bitorder="big")[:, :a.ncols]
+
+
+def from_dense(dense: np.ndarray, device=None) -> BitMatrix:
+    """core.py:417-432"""
+    dense = np.asarray(dense, dtype=np.uint8) & 1
+    if dense.ndim != 2:
+        raise DimensionError("from_dense expects a 2-D array")
+    nrows, ncols = dense.shape
+    w = words_per_row(ncols)
+    if nrows == 0 or ncols == 0:
+        return BitMatrix(nrows, ncols, device)
+    packed = np.packbits(dense, axis=1, bitorder="big")
+    if packed.shape[1] < w * 8:
+        packed = np.pad(packed, ((0, 0), (0, w * 8 - packed.shape[1])))
+    words = np.ascontiguousarray(packed).view(">u8").astype(np.uint64)
+    return from_numpy(words.reshape(nrows, w), ncols, device)
+
+
+# ------------------------------------------------------------ word ops
+def add_into(out: Mat, a: Mat, b: Mat) -> None:
+    """out = a XOR b; out may alias a or b (core.py:278-300)."""
+    _check_cuda_dev(out, a, b)
+    _lib.check(_lib.lib_cuda().gf2_add(out._view(), a._view(), b._view(),
+                                       _stream()))
+
+
+def add(a: Mat, b: Mat) -> BitMatrix:
+    """core.py:303-309"""
+    if a.shape != b.shape:
+        raise DimensionError(f"add shapes {a.shape} and {b.shape} differ")
+    out = BitMatrix(a.nrows, a.ncols, a.device)
+    add_into(out, a, b)
+    return out
+
+
+def copy_into(out: Mat, a: Mat) -> None:
+    """core.py:312-323 -- preserves bits beyond out's right edge."""
+    if out.shape != a.shape:
+        raise DimensionError(f"copy shapes {a.shape} -> {out.shape} differ")
+    _check_cuda_dev(out, a)
+    _lib.check(_lib.lib_cuda().gf2_copy(out._view(), a._view(), _stream()))
+
+
+def copy_out(w: Mat) -> BitMatrix:
+    """core.py:335-341 -- fresh owned copy with a clean tail."""
+    out = BitMatrix(w.nrows, w.ncols, w.device)
+    copy_into(out, w)
+    return out
+
+
+def zero_into(out: Mat) -> None:
+    _lib.check(_lib.lib_cuda().gf2_zero(out._view(), _stream()))
+
+
+def equal(a: Mat, b: Mat) -> bool:
+    """core.py:379-388 -- entry equality (tails masked), on device."""
+    if a.shape != b.shape:
+        return False
+    if a.nrows == 0 or a.width == 0:
+        return True
+    torch = _torch()
+    wa, wb = a.words, b.words
+    if wb.device != wa.device:
+        wb = wb.to(wa.device)
+    if not torch.equal(wa[:, :-1], wb[:, :-1]):
+        return False
+    tm = _signed(tail_mask(a.ncols))
+    return bool(torch.equal(wa[:, -1] & tm, wb[:, -1] & tm))
+
+
+def trailing_bits_clean(a: Mat) -> bool:
+    """core.py:435-440"""
+    if a.nrows == 0 or a.width == 0:
+        return True
+    spare = _signed(~tail_mask(a.ncols) & _FULL)
+    return not bool((a.words[:, -1] & spare).any())
+
+
+def first_difference(a: Mat, b: Mat):
+    """core.py:391-406 (via host copies)."""
+    if a.shape != b.shape:
+        raise DimensionError(f"shapes {a.shape} and {b.shape} differ")
+    if a.nrows == 0 or a.width == 0:
+        return None
+    diff = to_numpy(a) ^ to_numpy(b)
+    diff[:, -1] &= np.uint64(tail_mask(a.ncols))
+    rows = np.nonzero(diff.any(axis=1))[0]
+    if rows.size == 0:
+        return None
+    r = int(rows[0])
+    w = int(np.nonzero(diff[r])[0][0])
+    word = int(diff[r, w])
+    return (r, w * WORD_BITS + (WORD_BITS - word.bit_length()))

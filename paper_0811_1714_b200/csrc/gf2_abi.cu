@@ -1,0 +1,205 @@
+// C-ABI entry points (include/gf2b200.h). Validation mirrors the checks and
+// messages of the reference functions each entry replaces, so the Python
+// shim raises the same exception classes for the same inputs.
+#include <stdio.h>
+
+#include <string>
+
+#include "gf2_internal.cuh"
+
+namespace gf2 {
+int m4rm_mul(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accumulate, cudaStream_t s);
+int strassen_mul(const gf2_view &C, const gf2_view &A, const gf2_view &B, int64_t cutoff, int accumulate,
+                 cudaStream_t s);
+void peel_split(int64_t m, int64_t l, int64_t n, int64_t cutoff, int64_t out[4]);
+
+std::atomic<int64_t> g_launches{0};
+static thread_local std::string t_err;
+
+int set_error(int code, const std::string &msg) {
+    t_err = msg;
+    return code;
+}
+
+int check_cuda(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return GF2_OK;
+    return set_error(e == cudaErrorMemoryAllocation ? GF2_ERR_OOM : GF2_ERR_CUDA,
+                     std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static int check_view(const gf2_view *v, const char *name) {
+    if (!v) return set_error(GF2_ERR_PARAMETER, std::string(name) + ": null view");
+    if (v->nrows < 0 || v->ncols < 0)
+        return set_error(GF2_ERR_DIMENSION, std::string("negative dimensions ") + std::to_string(v->nrows) + "x" +
+                                                std::to_string(v->ncols));
+    const int64_t w = words_per_row(v->ncols);
+    if (v->nrows > 1 && v->pitch < w)
+        return set_error(GF2_ERR_PARAMETER, std::string(name) + ": pitch " + std::to_string(v->pitch) +
+                                                " < words per row " + std::to_string(w));
+    if (v->nrows > 0 && w > 0) {
+        if (!v->data) return set_error(GF2_ERR_PARAMETER, std::string(name) + ": null data");
+        if (reinterpret_cast<uintptr_t>(v->data) % 8)
+            return set_error(GF2_ERR_ALIGNMENT, std::string(name) + ": data not 8-byte (word) aligned");
+    }
+    return GF2_OK;
+}
+
+static bool overlaps(const gf2_view &x, const gf2_view &y) {
+    const int64_t wx = words_per_row(x.ncols), wy = words_per_row(y.ncols);
+    if (!x.nrows || !wx || !y.nrows || !wy) return false;
+    const uint64_t *x0 = x.data, *x1 = x.data + (x.nrows - 1) * x.pitch + wx;
+    const uint64_t *y0 = y.data, *y1 = y.data + (y.nrows - 1) * y.pitch + wy;
+    return x0 < y1 && y0 < x1;
+}
+
+static int check_mul(const gf2_view *c, const gf2_view *a, const gf2_view *b) {
+    GF2_TRY(check_view(a, "a"));
+    GF2_TRY(check_view(b, "b"));
+    GF2_TRY(check_view(c, "c"));
+    if (a->ncols != b->nrows)  // m4rm.py:70-73, strassen.py:260-262
+        return set_error(GF2_ERR_DIMENSION, "inner dimensions " + std::to_string(a->ncols) + " and " +
+                                                std::to_string(b->nrows) + " differ");
+    if (c->nrows != a->nrows || c->ncols != b->ncols)  // m4rm.py:82-84
+        return set_error(GF2_ERR_DIMENSION, "target " + std::to_string(c->nrows) + "x" +
+                                                std::to_string(c->ncols) + " != product " +
+                                                std::to_string(a->nrows) + "x" + std::to_string(b->ncols));
+    if (overlaps(*c, *a) || overlaps(*c, *b))  // schedule_winograd: c must not alias a or b
+        return set_error(GF2_ERR_PARAMETER, "product target aliases an operand");
+    return GF2_OK;
+}
+
+static int check_same_shape(const gf2_view *out, const gf2_view *a, const char *what) {
+    if (out->nrows != a->nrows || out->ncols != a->ncols)
+        return set_error(GF2_ERR_DIMENSION, std::string(what) + " shapes (" + std::to_string(a->nrows) + ", " +
+                                                std::to_string(a->ncols) + ") -> (" + std::to_string(out->nrows) +
+                                                ", " + std::to_string(out->ncols) + ") differ");
+    return GF2_OK;
+}
+
+}  // namespace gf2
+
+using namespace gf2;
+
+extern "C" {
+
+const char *gf2_version(void) { return "gf2b200 0.1.0 (sm_100a)"; }
+
+const char *gf2_last_error(void) { return t_err.c_str(); }
+
+int64_t gf2_pitch_words(int64_t ncols) {
+    int64_t w = words_per_row(ncols);
+    if (w >= 16) return (w + 15) / 16 * 16;
+    return (w + 1) / 2 * 2;
+}
+
+int64_t gf2_launch_count(void) { return g_launches.load(); }
+
+int gf2_timer_enable(int on) { return timer_enable(on); }
+
+int gf2_timer_read(double *kernel_ms, double *bitops, int64_t *launches) {
+    return timer_read(kernel_ms, bitops, launches);
+}
+
+int gf2_alloc(int64_t nrows, int64_t ncols, gf2_view *out, void *stream) {
+    if (!out) return set_error(GF2_ERR_PARAMETER, "null output view");
+    if (nrows < 0 || ncols < 0)
+        return set_error(GF2_ERR_DIMENSION,
+                         "negative dimensions " + std::to_string(nrows) + "x" + std::to_string(ncols));
+    const int64_t pitch = gf2_pitch_words(ncols);
+    size_t bytes = (size_t)(nrows * pitch) * 8;
+    void *p = nullptr;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (bytes) {
+        GF2_TRY(check_cuda(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync"));
+        GF2_TRY(check_cuda(cudaMemsetAsync(p, 0, bytes, s), "cudaMemsetAsync"));
+    }
+    out->data = (uint64_t *)p;
+    out->pitch = pitch;
+    out->nrows = nrows;
+    out->ncols = ncols;
+    return GF2_OK;
+}
+
+int gf2_free(gf2_view *v, void *stream) {
+    if (!v) return GF2_OK;
+    if (v->data) GF2_TRY(check_cuda(cudaFreeAsync(v->data, (cudaStream_t)stream), "cudaFreeAsync"));
+    v->data = nullptr;
+    return GF2_OK;
+}
+
+int gf2_upload(const gf2_view *dst, const uint64_t *host, int64_t host_stride, void *stream) {
+    GF2_TRY(check_view(dst, "dst"));
+    const int64_t w = words_per_row(dst->ncols);
+    if (!dst->nrows || !w) return GF2_OK;
+    if (!host || host_stride < w) return set_error(GF2_ERR_PARAMETER, "bad host buffer / stride");
+    return check_cuda(cudaMemcpy2DAsync(dst->data, dst->pitch * 8, host, host_stride * 8, w * 8, dst->nrows,
+                                        cudaMemcpyHostToDevice, (cudaStream_t)stream),
+                      "upload");
+}
+
+int gf2_download(const gf2_view *src, uint64_t *host, int64_t host_stride, void *stream) {
+    GF2_TRY(check_view(src, "src"));
+    const int64_t w = words_per_row(src->ncols);
+    if (!src->nrows || !w) return GF2_OK;
+    if (!host || host_stride < w) return set_error(GF2_ERR_PARAMETER, "bad host buffer / stride");
+    return check_cuda(cudaMemcpy2DAsync(host, host_stride * 8, src->data, src->pitch * 8, w * 8, src->nrows,
+                                        cudaMemcpyDeviceToHost, (cudaStream_t)stream),
+                      "download");
+}
+
+int gf2_zero(const gf2_view *dst, void *stream) {
+    GF2_TRY(check_view(dst, "dst"));
+    return launch_ewise(*dst, nullptr, nullptr, 0, (cudaStream_t)stream);
+}
+
+int gf2_random(const gf2_view *dst, uint64_t seed, int64_t row_base, void *stream) {
+    GF2_TRY(check_view(dst, "dst"));
+    return launch_random(*dst, seed, row_base, (cudaStream_t)stream);
+}
+
+int gf2_bernoulli(const gf2_view *dst, uint64_t seed, uint64_t threshold, int64_t row_base, void *stream) {
+    GF2_TRY(check_view(dst, "dst"));
+    return launch_bernoulli(*dst, seed, threshold, row_base, (cudaStream_t)stream);
+}
+
+int gf2_add(const gf2_view *out, const gf2_view *a, const gf2_view *b, void *stream) {
+    GF2_TRY(check_view(out, "out"));
+    GF2_TRY(check_view(a, "a"));
+    GF2_TRY(check_view(b, "b"));
+    if (a->nrows != b->nrows || a->ncols != b->ncols || out->nrows != a->nrows || out->ncols != a->ncols)
+        return set_error(GF2_ERR_DIMENSION, "add shapes (" + std::to_string(a->nrows) + ", " +
+                                                std::to_string(a->ncols) + "), (" + std::to_string(b->nrows) +
+                                                ", " + std::to_string(b->ncols) + ") -> (" +
+                                                std::to_string(out->nrows) + ", " + std::to_string(out->ncols) +
+                                                ") differ");
+    return launch_ewise(*out, a, b, 2, (cudaStream_t)stream);
+}
+
+int gf2_copy(const gf2_view *out, const gf2_view *a, void *stream) {
+    GF2_TRY(check_view(out, "out"));
+    GF2_TRY(check_view(a, "a"));
+    GF2_TRY(check_same_shape(out, a, "copy"));
+    return launch_ewise(*out, a, nullptr, 1, (cudaStream_t)stream);
+}
+
+int gf2_m4rm(const gf2_view *c, const gf2_view *a, const gf2_view *b, int k, int accumulate, void *stream) {
+    if (k < 1 || k > 16) return set_error(GF2_ERR_PARAMETER, "k=" + std::to_string(k) + " outside 1..16");
+    GF2_TRY(check_mul(c, a, b));
+    return m4rm_mul(*c, *a, *b, accumulate ? 1 : 0, (cudaStream_t)stream);
+}
+
+int gf2_strassen(const gf2_view *c, const gf2_view *a, const gf2_view *b, int64_t cutoff, int k, int accumulate,
+                 void *stream) {
+    if (cutoff < 64) return set_error(GF2_ERR_PARAMETER, "cutoff " + std::to_string(cutoff) + " < 64");
+    if (k < 0 || k > 16) return set_error(GF2_ERR_PARAMETER, "k=" + std::to_string(k) + " outside 0..16");
+    GF2_TRY(check_mul(c, a, b));
+    return strassen_mul(*c, *a, *b, cutoff, accumulate ? 1 : 0, (cudaStream_t)stream);
+}
+
+int gf2_peel_split(int64_t m, int64_t l, int64_t n, int64_t cutoff, int64_t out4[4]) {
+    if (!out4) return set_error(GF2_ERR_PARAMETER, "null output");
+    peel_split(m, l, n, cutoff, out4);
+    return GF2_OK;
+}
+
+}  // extern "C"

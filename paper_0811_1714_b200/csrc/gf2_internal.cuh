@@ -1,0 +1,88 @@
+// Internal declarations shared by the gf2b200 translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/gf2b200.h"
+
+namespace gf2 {
+
+typedef uint64_t u64;
+
+constexpr int kWordBits = 64;
+
+__host__ __device__ inline int64_t words_per_row(int64_t ncols) {
+    return (ncols + kWordBits - 1) / kWordBits;
+}
+// core.py:49-54
+__host__ __device__ inline u64 tail_mask(int64_t ncols) {
+    int64_t rem = ncols % kWordBits;
+    return rem == 0 ? ~0ULL : (~0ULL << (kWordBits - rem));
+}
+
+// Status plumbing ------------------------------------------------------
+int set_error(int code, const std::string &msg);
+int check_cuda(cudaError_t e, const char *what);
+extern std::atomic<int64_t> g_launches;
+inline void note_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+#define GF2_TRY(expr)                  \
+    do {                               \
+        int _rc = (expr);              \
+        if (_rc != GF2_OK) return _rc; \
+    } while (0)
+
+// A view with offsets (window of a window) resolved on the host.
+inline gf2_view sub_view(const gf2_view &v, int64_t r0, int64_t c0, int64_t nr, int64_t nc) {
+    gf2_view o;
+    o.data = v.data + r0 * v.pitch + c0 / kWordBits;
+    o.pitch = v.pitch;
+    o.nrows = nr;
+    o.ncols = nc;
+    return o;
+}
+
+// Launchers (all asynchronous on `s`) ---------------------------------
+int launch_random(const gf2_view &v, u64 seed, int64_t row_base, cudaStream_t s);
+int launch_bernoulli(const gf2_view &v, u64 seed, u64 thresh, int64_t row_base, cudaStream_t s);
+int launch_ewise(const gf2_view &out, const gf2_view *a, const gf2_view *b, int op, cudaStream_t s);
+
+// Batched XOR-combine used by the breadth-first Strassen-Winograd:
+// for output o = p * nq + q (p < nprob, q < nq):
+//   dst(p, q) [R x W words] (^)= XOR_{i in mask[q]} src(p, i)
+// with dst(p,q) = dst + p*dst_stride + dst_off[q], src(p,i) = src + p*src_stride + src_off[i].
+struct CombineArgs {
+    const u64 *src;
+    int64_t src_pitch, src_stride;
+    int64_t src_off[8];
+    u64 *dst;
+    int64_t dst_pitch, dst_stride;
+    int64_t dst_off[8];
+    unsigned mask[8];
+    int nq;
+    int64_t R, W;
+    int64_t nprob;
+    int accumulate;
+};
+int launch_combine(const CombineArgs &a, cudaStream_t s);
+
+// Batched M4RM: problem q uses A + q*sa, B + q*sb, C + q*sc (same dims).
+struct M4rmBatch {
+    const u64 *A;
+    int64_t pa, sa;
+    const u64 *B;
+    int64_t pb, sb;
+    u64 *C;
+    int64_t pc, sc;
+    int64_t m, l, n;
+    int64_t nprob;
+    int accumulate;
+};
+int launch_m4rm(const M4rmBatch &b, cudaStream_t s);
+int timer_enable(int on);
+int timer_read(double *ms, double *bitops, int64_t *launches);
+
+}  // namespace gf2

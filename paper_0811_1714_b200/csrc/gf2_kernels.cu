@@ -1,0 +1,167 @@
+// Word-wise kernels: generators, masked add/copy/zero, and the batched
+// XOR-combine behind the breadth-first Strassen-Winograd schedule.
+// All are HBM-bound streaming kernels: one 64-bit word per thread, warps
+// running along a row so every access is a coalesced 256-byte segment.
+#include "gf2_internal.cuh"
+
+namespace gf2 {
+
+namespace {
+
+constexpr u64 kGolden = 0x9E3779B97F4A7C15ULL;
+
+__device__ __forceinline__ u64 splitmix_mix(u64 z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// Write `v` into word j of a row of a view whose last word is `last`,
+// preserving bits beyond the right edge (core.py:298-300, 320-323).
+__device__ __forceinline__ void put_word(u64 *p, int64_t j, int64_t last, u64 tm, u64 v) {
+    if (j == last && tm != ~0ULL)
+        p[j] = (p[j] & ~tm) | (v & tm);
+    else
+        p[j] = v;
+}
+
+// core.py:191-208 -- word (r, j) = splitmix over flat index (row_base+r)*width+j.
+__global__ void k_random(u64 *data, int64_t pitch, int64_t nrows, int64_t width, u64 tm,
+                         u64 seed, int64_t row_base) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= width) return;
+    for (int64_t r = (int64_t)blockIdx.y * blockDim.y + threadIdx.y; r < nrows;
+         r += (int64_t)gridDim.y * blockDim.y) {
+        u64 idx = (u64)((row_base + r) * width + j) + 1ULL;
+        u64 v = splitmix_mix(seed + idx * kGolden);
+        put_word(data + r * pitch, j, width - 1, tm, v);
+    }
+}
+
+// bit (r, c) = [splitmix(seed + (e+1)*golden) < T], e = (row_base+r)*ncols + c.
+__global__ void k_bernoulli(u64 *data, int64_t pitch, int64_t nrows, int64_t ncols, int64_t width,
+                            u64 tm, u64 seed, u64 thresh, int64_t row_base) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= width) return;
+    for (int64_t r = (int64_t)blockIdx.y * blockDim.y + threadIdx.y; r < nrows;
+         r += (int64_t)gridDim.y * blockDim.y) {
+        u64 e0 = (u64)((row_base + r) * ncols + j * kWordBits) + 1ULL;
+        int nb = (int)min((int64_t)kWordBits, ncols - j * kWordBits);
+        u64 v = 0;
+        u64 x = seed + e0 * kGolden;
+#pragma unroll 8
+        for (int b = 0; b < nb; ++b) {
+            u64 z = splitmix_mix(x);
+            v |= (u64)(z < thresh) << (63 - b);
+            x += kGolden;
+        }
+        put_word(data + r * pitch, j, width - 1, tm, v);
+    }
+}
+
+// op 0: out = 0; op 1: out = a; op 2: out = a ^ b (core.py:278-323).
+template <int OP>
+__global__ void k_ewise(u64 *out, int64_t po, const u64 *a, int64_t pa, const u64 *b, int64_t pb,
+                        int64_t nrows, int64_t width, u64 tm) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= width) return;
+    for (int64_t r = (int64_t)blockIdx.y * blockDim.y + threadIdx.y; r < nrows;
+         r += (int64_t)gridDim.y * blockDim.y) {
+        u64 v = 0;
+        if (OP >= 1) v = a[r * pa + j];
+        if (OP == 2) v ^= b[r * pb + j];
+        put_word(out + r * po, j, width - 1, tm, v);
+    }
+}
+
+__global__ void k_combine(CombineArgs p, int64_t wblocks) {
+    int64_t o = blockIdx.x / wblocks;
+    int64_t j = (blockIdx.x % wblocks) * blockDim.x + threadIdx.x;
+    if (j >= p.W) return;
+    int64_t prob = o / p.nq;
+    int q = (int)(o % p.nq);
+    unsigned mask = p.mask[q];
+    const u64 *sbase = p.src + prob * p.src_stride;
+    u64 *d = p.dst + prob * p.dst_stride + p.dst_off[q];
+    for (int64_t r = (int64_t)blockIdx.y * blockDim.y + threadIdx.y; r < p.R;
+         r += (int64_t)gridDim.y * blockDim.y) {
+        u64 v = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (mask & (1u << i)) v ^= __ldg(sbase + p.src_off[i] + r * p.src_pitch + j);
+        u64 *dp = d + r * p.dst_pitch + j;
+        if (p.accumulate)
+            *dp ^= v;
+        else
+            *dp = v;
+    }
+}
+
+inline dim3 row_grid(int64_t width, int64_t nrows, dim3 blk) {
+    int64_t gx = (width + blk.x - 1) / blk.x;
+    int64_t gy = (nrows + blk.y - 1) / blk.y;
+    if (gy > 65535) gy = 65535;
+    if (gy < 1) gy = 1;
+    return dim3((unsigned)gx, (unsigned)gy, 1);
+}
+
+inline dim3 row_block(int64_t width) {
+    // warps along the row; short rows get more rows per block
+    if (width >= 128) return dim3(128, 2, 1);
+    if (width >= 32) return dim3(32, 8, 1);
+    return dim3(8, 32, 1);
+}
+
+}  // namespace
+
+int launch_random(const gf2_view &v, u64 seed, int64_t row_base, cudaStream_t s) {
+    int64_t width = words_per_row(v.ncols);
+    if (!width || !v.nrows) return GF2_OK;
+    dim3 blk = row_block(width);
+    k_random<<<row_grid(width, v.nrows, blk), blk, 0, s>>>(v.data, v.pitch, v.nrows, width,
+                                                         tail_mask(v.ncols), seed, row_base);
+    note_launch();
+    return check_cuda(cudaGetLastError(), "k_random launch");
+}
+
+int launch_bernoulli(const gf2_view &v, u64 seed, u64 thresh, int64_t row_base, cudaStream_t s) {
+    int64_t width = words_per_row(v.ncols);
+    if (!width || !v.nrows) return GF2_OK;
+    dim3 blk = row_block(width);
+    k_bernoulli<<<row_grid(width, v.nrows, blk), blk, 0, s>>>(
+        v.data, v.pitch, v.nrows, v.ncols, width, tail_mask(v.ncols), seed, thresh, row_base);
+    note_launch();
+    return check_cuda(cudaGetLastError(), "k_bernoulli launch");
+}
+
+int launch_ewise(const gf2_view &out, const gf2_view *a, const gf2_view *b, int op, cudaStream_t s) {
+    int64_t width = words_per_row(out.ncols);
+    if (!width || !out.nrows) return GF2_OK;
+    dim3 blk = row_block(width);
+    dim3 grd = row_grid(width, out.nrows, blk);
+    u64 tm = tail_mask(out.ncols);
+    if (op == 0)
+        k_ewise<0><<<grd, blk, 0, s>>>(out.data, out.pitch, nullptr, 0, nullptr, 0, out.nrows, width, tm);
+    else if (op == 1)
+        k_ewise<1><<<grd, blk, 0, s>>>(out.data, out.pitch, a->data, a->pitch, nullptr, 0, out.nrows,
+                                       width, tm);
+    else
+        k_ewise<2><<<grd, blk, 0, s>>>(out.data, out.pitch, a->data, a->pitch, b->data, b->pitch,
+                                       out.nrows, width, tm);
+    note_launch();
+    return check_cuda(cudaGetLastError(), "k_ewise launch");
+}
+
+int launch_combine(const CombineArgs &a, cudaStream_t s) {
+    if (!a.R || !a.W || !a.nprob) return GF2_OK;
+    dim3 blk = row_block(a.W);
+    int64_t wblocks = (a.W + blk.x - 1) / blk.x;
+    int64_t gx = wblocks * a.nprob * a.nq;
+    int64_t gy = (a.R + blk.y - 1) / blk.y;
+    if (gy > 65535) gy = 65535;
+    k_combine<<<dim3((unsigned)gx, (unsigned)gy, 1), blk, 0, s>>>(a, wblocks);
+    note_launch();
+    return check_cuda(cudaGetLastError(), "k_combine launch");
+}
+
+}  // namespace gf2

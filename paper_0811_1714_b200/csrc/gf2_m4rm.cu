@@ -1,0 +1,362 @@
+// M4RM ("Method of the Four Russians") multiply on sm_100a: C (^)= A.B.
+//
+// Restates m4rm.py:77-121 (`_mul_into`) + graycode.py:108-156
+// (`make_table`) for the B200 memory hierarchy:
+//
+//   * A CTA owns a C tile of BM = 32*RPT rows x 1024 columns (16 words) and
+//     keeps it in registers for the whole K loop: each thread holds a
+//     128-bit column slice of RPT rows (8 lanes = one 128-byte row, so the
+//     4 quarter-warps of a warp cover 4 rows per instruction).
+//   * K advances one 64-bit word of A (64 rows of B) per stage. The B panel
+//     (64 rows x 1024 columns, 8 KiB) and the A column words (BM x 8 B) of
+//     the NEXT stage are prefetched with cp.async while the current stage is
+//     consumed (double-buffered).
+//   * Each half stage (32 rows of B) builds 4 Gray-code tables of 2^8 rows
+//     x 1024 bits (4 x 32 KiB) in shared memory. Table j, slot x holds the
+//     XOR of rows i of the 8-row group with bit (7-i) of x set -- exactly
+//     the reference's big-endian CombinationTable (graycode.py:78-105).
+//     Every thread builds 32 slots of one 128-bit column slice by a
+//     Gray walk held in registers, so the build costs one 16-byte shared
+//     store per slot and no shared-memory reads beyond the 8 source rows.
+//   * Lookups: for every row, the 4 bytes of the A half-word index the 4
+//     tables (MSB-first, m4rm.py:54-66); 8 lanes read one 128-byte table row
+//     as LDS.128 -- conflict-free for any index -- and XOR it into the
+//     register accumulator.
+//   * Epilogue: masked store (bits beyond the window edge preserved),
+//     XOR-accumulate, or red.global.xor for split-K (order-independent, so
+//     deterministic).
+//
+// Roofline: each lookup moves 16 B of shared memory per lane and applies 8
+// rows of B to 128 columns (1024 bit-ops / 16 B = 64 bit-ops per byte);
+// table builds add 2^8/BM of that traffic. The kernel is bound by the
+// 128 B/clk/SM shared-memory crossbar.
+#include <vector>
+
+#include "gf2_internal.cuh"
+
+namespace gf2 {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kTables = 4;      // 8-bit tables per half stage (32 rows of B)
+constexpr int kTabRows = 256;   // 2^8 slots
+constexpr int kTileWords = 16;  // 1024 columns per C tile
+constexpr int kRowBytes = kTileWords * 8;
+constexpr int kTableBytes = kTabRows * kRowBytes;     // 32 KiB
+constexpr int kStageRows = 64;                         // rows of B per stage
+constexpr int kBStageBytes = kStageRows * kRowBytes;  // 8 KiB
+
+template <int RPT>
+constexpr int smem_bytes() {
+    return kTables * kTableBytes + 2 * kBStageBytes + 2 * (32 * RPT) * 8;
+}
+
+struct KArgs {
+    const u64 *A;
+    int64_t pa, sa;
+    const u64 *B;
+    int64_t pb, sb;
+    u64 *C;
+    int64_t pc, sc;
+    int64_t m, l, n;
+    int64_t Wl, Wn;
+    int64_t kws;  // A words per split
+    int nsplit;
+    int mode;  // 0 store, 1 xor, 2 atomic xor
+};
+
+__device__ __forceinline__ void cp_async8(uint32_t saddr, const void *g, bool pred) {
+    int sz = pred ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(g), "r"(sz)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+__device__ __forceinline__ void sts128(uint32_t addr, u64 a, u64 b) {
+    asm volatile("st.shared.v2.u64 [%0], {%1, %2};\n" ::"r"(addr), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void lds128(uint32_t addr, u64 &a, u64 &b) {
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];\n" : "=l"(a), "=l"(b) : "r"(addr));
+}
+
+template <int RPT>
+__global__ void __launch_bounds__(kThreads, 1) k_m4rm(KArgs p) {
+    constexpr int BM = 32 * RPT;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const uint32_t s_tab = (uint32_t)__cvta_generic_to_shared(smem);
+    const uint32_t s_bst = s_tab + kTables * kTableBytes;
+    const uint32_t s_ast = s_bst + 2 * kBStageBytes;
+    const u64 *a_st = reinterpret_cast<const u64 *>(smem + kTables * kTableBytes + 2 * kBStageBytes);
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int s = lane & 7;                    // 128-bit column slice
+    const int rg = (tid >> 5) * 4 + (lane >> 3);  // row group 0..31
+
+    const int64_t prob = blockIdx.z / p.nsplit;
+    const int split = blockIdx.z % p.nsplit;
+    const int64_t col_w0 = (int64_t)blockIdx.x * kTileWords;
+    const int64_t row0 = (int64_t)blockIdx.y * BM;
+    const u64 *A = p.A + prob * p.sa;
+    const u64 *B = p.B + prob * p.sb;
+    u64 *C = p.C + prob * p.sc;
+
+    const int64_t kw0 = (int64_t)split * p.kws;
+    const int64_t kw1 = min(kw0 + p.kws, p.Wl);
+    const u64 atm = tail_mask(p.l);
+
+    // masks for this thread's two B words (tail of a ragged / windowed B)
+    const int64_t wj0 = col_w0 + 2 * s;
+    const u64 bm0 = (wj0 == p.Wn - 1) ? tail_mask(p.n) : ~0ULL;
+    const u64 bm1 = (wj0 + 1 == p.Wn - 1) ? tail_mask(p.n) : ~0ULL;
+
+    auto load_stage = [&](int64_t kw, int buf) {
+        // B panel: 64 rows x 16 words
+#pragma unroll
+        for (int i = 0; i < (kStageRows * kTileWords) / kThreads; ++i) {
+            int e = tid + kThreads * i;
+            int r = e >> 4, wd = e & 15;
+            int64_t brow = kw * 64 + r;
+            bool ok = (brow < p.l) && (col_w0 + wd < p.Wn);
+            const u64 *src = ok ? (B + brow * p.pb + col_w0 + wd) : B;
+            cp_async8(s_bst + buf * kBStageBytes + r * kRowBytes + wd * 8, src, ok);
+        }
+        // A column words for the BM rows
+#pragma unroll
+        for (int i = 0; i < (BM + kThreads - 1) / kThreads; ++i) {
+            int r = tid + kThreads * i;
+            if (r < BM) {
+                bool ok = row0 + r < p.m;
+                const u64 *src = ok ? (A + (row0 + r) * p.pa + kw) : A;
+                cp_async8(s_ast + (buf * BM + r) * 8, src, ok);
+            }
+        }
+        cp_async_commit();
+    };
+
+    u64 acc[RPT][2];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) acc[i][0] = acc[i][1] = 0ULL;
+
+    // table-build role: table tj, slots [r0*32, r0*32+32), slice s
+    const int tj = rg >> 3, r0 = rg & 7;
+
+    if (kw0 < kw1) load_stage(kw0, 0);
+    for (int64_t kw = kw0; kw < kw1; ++kw) {
+        const int buf = (int)((kw - kw0) & 1);
+        cp_async_wait_all();
+        __syncthreads();  // stage kw visible; previous lookups finished
+        if (kw + 1 < kw1) load_stage(kw + 1, buf ^ 1);
+        const u64 amask = (kw == p.Wl - 1) ? atm : ~0ULL;
+
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (h == 1) __syncthreads();  // lookups of half 0 done before rebuild
+            // ---- build table tj from B rows 32h + 8tj + (0..7), slice s
+            {
+                u64 x0[8], x1[8];
+                const uint32_t srow = s_bst + buf * kBStageBytes + (32 * h + 8 * tj) * kRowBytes + s * 16;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    lds128(srow + i * kRowBytes, x0[i], x1[i]);
+                    x0[i] &= bm0;
+                    x1[i] &= bm1;
+                }
+                u64 c0 = 0, c1 = 0;
+                if (r0 & 4) { c0 ^= x0[0]; c1 ^= x1[0]; }
+                if (r0 & 2) { c0 ^= x0[1]; c1 ^= x1[1]; }
+                if (r0 & 1) { c0 ^= x0[2]; c1 ^= x1[2]; }
+                const uint32_t tbase = s_tab + tj * kTableBytes + (r0 * 32) * kRowBytes + s * 16;
+                sts128(tbase, c0, c1);
+#pragma unroll
+                for (int i = 1; i < 32; ++i) {
+                    const int b = (i & 1) ? 0 : (i & 2) ? 1 : (i & 4) ? 2 : (i & 8) ? 3 : 4;  // flipped Gray bit
+                    const int g = i ^ (i >> 1);
+                    c0 ^= x0[7 - b];                  // slot bit b <-> source row 7-b
+                    c1 ^= x1[7 - b];
+                    sts128(tbase + g * kRowBytes, c0, c1);
+                }
+            }
+            __syncthreads();
+            // ---- lookups
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                u64 a = a_st[buf * BM + i * 32 + rg] & amask;
+                uint32_t hw = (h == 0) ? (uint32_t)(a >> 32) : (uint32_t)a;
+                u64 v0, v1, w0, w1;
+                const uint32_t base = s_tab + s * 16;
+                lds128(base + 0 * kTableBytes + ((hw >> 24) & 0xFF) * kRowBytes, v0, v1);
+                lds128(base + 1 * kTableBytes + ((hw >> 16) & 0xFF) * kRowBytes, w0, w1);
+                acc[i][0] ^= v0 ^ w0;
+                acc[i][1] ^= v1 ^ w1;
+                lds128(base + 2 * kTableBytes + ((hw >> 8) & 0xFF) * kRowBytes, v0, v1);
+                lds128(base + 3 * kTableBytes + (hw & 0xFF) * kRowBytes, w0, w1);
+                acc[i][0] ^= v0 ^ w0;
+                acc[i][1] ^= v1 ^ w1;
+            }
+        }
+    }
+
+    // ---- epilogue
+    const u64 ctm = tail_mask(p.n);
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+        const int64_t row = row0 + i * 32 + rg;
+        if (row >= p.m) continue;
+        u64 *crow = C + row * p.pc;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int64_t wi = wj0 + e;
+            if (wi >= p.Wn) continue;
+            const u64 v = acc[i][e];
+            if (p.mode == 2) {
+                if (v) atomicXor(reinterpret_cast<unsigned long long *>(crow + wi), (unsigned long long)v);
+            } else if (p.mode == 1) {
+                crow[wi] ^= v;
+            } else if (wi == p.Wn - 1 && ctm != ~0ULL) {
+                crow[wi] = (crow[wi] & ~ctm) | v;
+            } else {
+                crow[wi] = v;
+            }
+        }
+    }
+}
+
+template <int RPT>
+int launch_rpt(const KArgs &ka, int64_t col_tiles, int64_t row_tiles, int64_t zdim, cudaStream_t s) {
+    static bool configured = false;
+    constexpr int sm = smem_bytes<RPT>();
+    if (!configured) {
+        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_m4rm<RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+                           "cudaFuncSetAttribute(k_m4rm)"));
+        configured = true;
+    }
+    dim3 grid((unsigned)col_tiles, (unsigned)row_tiles, (unsigned)zdim);
+    k_m4rm<RPT><<<grid, kThreads, sm, s>>>(ka);
+    note_launch();
+    return check_cuda(cudaGetLastError(), "k_m4rm launch");
+}
+
+int g_num_sms = 0;
+
+// kernel timer (gf2_timer_*): event pairs around each M4RM launch
+struct TimedLaunch {
+    cudaEvent_t a, b;
+    double bitops;
+};
+bool g_timing = false;
+std::vector<TimedLaunch> g_timed;
+std::vector<cudaEvent_t> g_event_pool;
+
+cudaEvent_t pool_event() {
+    if (!g_event_pool.empty()) {
+        cudaEvent_t e = g_event_pool.back();
+        g_event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+}  // namespace
+
+int timer_enable(int on) {
+    for (auto &t : g_timed) {
+        g_event_pool.push_back(t.a);
+        g_event_pool.push_back(t.b);
+    }
+    g_timed.clear();
+    g_timing = on != 0;
+    return GF2_OK;
+}
+
+int timer_read(double *ms, double *bitops, int64_t *launches) {
+    double tot = 0, ops = 0;
+    for (auto &t : g_timed) {
+        GF2_TRY(check_cuda(cudaEventSynchronize(t.b), "timer sync"));
+        float e = 0;
+        GF2_TRY(check_cuda(cudaEventElapsedTime(&e, t.a, t.b), "timer elapsed"));
+        tot += e;
+        ops += t.bitops;
+    }
+    if (ms) *ms = tot;
+    if (bitops) *bitops = ops;
+    if (launches) *launches = (int64_t)g_timed.size();
+    return GF2_OK;
+}
+
+int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
+    if (!b.m || !b.n || !b.nprob) return GF2_OK;
+    const int64_t Wn = words_per_row(b.n), Wl = words_per_row(b.l);
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    auto zero_c = [&]() -> int {
+        if (b.nprob == 1 || b.sc == b.m * b.pc) {
+            gf2_view v{b.C, b.pc, b.m * b.nprob, b.n};
+            return launch_ewise(v, nullptr, nullptr, 0, s);
+        }
+        for (int64_t q = 0; q < b.nprob; ++q) {
+            gf2_view v{b.C + q * b.sc, b.pc, b.m, b.n};
+            GF2_TRY(launch_ewise(v, nullptr, nullptr, 0, s));
+        }
+        return GF2_OK;
+    };
+    if (b.l == 0) return b.accumulate ? GF2_OK : zero_c();
+
+    const int64_t col_tiles = (Wn + kTileWords - 1) / kTileWords;
+    const int64_t want = g_num_sms;  // one CTA per SM is resident (smem-bound)
+    int rpt = 16;
+    int64_t row_tiles = (b.m + 32 * rpt - 1) / (32 * rpt);
+    while (rpt > 4 && row_tiles * col_tiles * b.nprob < want) {
+        rpt /= 2;
+        row_tiles = (b.m + 32 * rpt - 1) / (32 * rpt);
+    }
+    const int64_t tiles = row_tiles * col_tiles * b.nprob;
+    int nsplit = 1;
+    if (tiles < want) {
+        int64_t ns = (want + tiles - 1) / tiles;
+        if (ns > Wl) ns = Wl;
+        nsplit = (int)ns;
+    }
+    int64_t kws = (Wl + nsplit - 1) / nsplit;
+    nsplit = (int)((Wl + kws - 1) / kws);
+    if ((int64_t)nsplit * b.nprob > 65535 || row_tiles > 65535)
+        return set_error(GF2_ERR_PARAMETER, "m4rm grid too large");
+
+    KArgs ka{b.A, b.pa, b.sa, b.B, b.pb, b.sb, b.C, b.pc, b.sc, b.m, b.l, b.n, Wl, Wn, kws, nsplit, 0};
+    if (nsplit > 1) {
+        if (!b.accumulate) GF2_TRY(zero_c());
+        ka.mode = 2;
+    } else {
+        ka.mode = b.accumulate ? 1 : 0;
+    }
+    const int64_t z = (int64_t)nsplit * b.nprob;
+    TimedLaunch tl{};
+    if (g_timing) {
+        tl.a = pool_event();
+        tl.b = pool_event();
+        tl.bitops = (double)b.m * (double)b.l * (double)b.n * (double)b.nprob;
+        cudaEventRecord(tl.a, s);
+    }
+    int rc;
+    if (rpt == 16)
+        rc = launch_rpt<16>(ka, col_tiles, row_tiles, z, s);
+    else if (rpt == 8)
+        rc = launch_rpt<8>(ka, col_tiles, row_tiles, z, s);
+    else
+        rc = launch_rpt<4>(ka, col_tiles, row_tiles, z, s);
+    if (g_timing) {
+        cudaEventRecord(tl.b, s);
+        g_timed.push_back(tl);
+    }
+    return rc;
+}
+
+}  // namespace gf2

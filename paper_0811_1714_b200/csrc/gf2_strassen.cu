@@ -1,0 +1,217 @@
+// Strassen-Winograd over GF(2) on device windows, breadth first.
+//
+// Same mathematics as strassen.py:141-204 (7 products, 15 additions per
+// level, Winograd's schedule) and the same peeling (strassen.py:66-84,
+// 219-249), re-scheduled for a GPU: instead of walking the recursion tree
+// depth first with two scratch quadrants per level (a CPU cache design),
+// every level is one batched launch.
+//
+//   level s -> s+1 (pre):  for every level-s problem p and product i,
+//       A_{s+1}[7p+i] = XOR of A_s[p]'s quadrants in SA[i]   (one launch)
+//       B_{s+1}[7p+i] = XOR of B_s[p]'s quadrants in SB[i]   (one launch)
+//   leaves: all 7^d products in ONE batched M4RM launch
+//   level s+1 -> s (post): C_s[p] quadrant Q = XOR of C_{s+1}[7p+i], i in SC[Q]
+//
+// Over GF(2) every S/T/U step of the schedule is an XOR, so Winograd's
+// operand sums and output combination reduce to these subset tables
+// (derived from the 22-step schedule, strassen.py:183-204):
+//   P1 = A11.B11                     -> C11 C12 C21 C22
+//   P2 = A12.B21                     -> C11
+//   P3 = (A11+A12+A21+A22).B22       -> C12
+//   P4 = A22.(B11+B12+B21+B22)       -> C21
+//   P5 = (A21+A22).(B11+B12)         -> C12 C22
+//   P6 = (A11+A21+A22).(B11+B12+B22) -> C12 C21 C22
+//   P7 = (A11+A21).(B12+B22)         -> C21 C22
+// HBM is plentiful (180 GB), so every level's operands get their own
+// buffers (stream-ordered pool) and the 7^d leaf products run concurrently.
+#include "gf2_internal.cuh"
+
+namespace gf2 {
+
+namespace {
+// quadrant bits: 1 = X11, 2 = X12, 4 = X21, 8 = X22
+constexpr unsigned kSA[7] = {1, 2, 15, 8, 12, 13, 5};
+constexpr unsigned kSB[7] = {1, 4, 8, 15, 3, 11, 10};
+// product bits: 1 << (i-1) for P_i
+constexpr unsigned kSC[4] = {0x03, 0x35, 0x69, 0x71};
+
+bool g_pool_configured = false;
+
+int pool_setup() {
+    if (g_pool_configured) return GF2_OK;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thresh = UINT64_MAX;  // keep freed blocks cached in the pool
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh);
+    }
+    cudaGetLastError();
+    g_pool_configured = true;
+    return GF2_OK;
+}
+
+int m4rm_view(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accumulate, cudaStream_t s) {
+    M4rmBatch mb{a.data, a.pitch, 0, b.data, b.pitch, 0, c.data, c.pitch, 0,
+                 a.nrows,  a.ncols, b.ncols, 1, accumulate};
+    return launch_m4rm(mb, s);
+}
+
+int strassen_core(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0, int depth, int accumulate,
+                  cudaStream_t s) {
+    int64_t M[24], L[24], N[24], Lw[24], Nw[24], P[24];
+    for (int i = 0; i <= depth; ++i) {
+        M[i] = A0.nrows >> i;
+        L[i] = A0.ncols >> i;
+        N[i] = B0.ncols >> i;
+        Lw[i] = L[i] / kWordBits;
+        Nw[i] = N[i] / kWordBits;
+        P[i] = i == 0 ? 1 : P[i - 1] * 7;
+    }
+    // workspace: per level s >= 1, A_s, B_s and C_s for all 7^s problems
+    int64_t offA[24], offB[24], offC[24], total = 0;
+    for (int i = 1; i <= depth; ++i) {
+        offA[i] = total;
+        total += P[i] * M[i] * Lw[i];
+        offB[i] = total;
+        total += P[i] * L[i] * Nw[i];
+        offC[i] = total;
+        total += P[i] * M[i] * Nw[i];
+    }
+    GF2_TRY(pool_setup());
+    u64 *ws = nullptr;
+    cudaError_t e = cudaMallocAsync((void **)&ws, (size_t)total * 8, s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(GF2_ERR_OOM, std::string("strassen workspace: ") + cudaGetErrorString(e));
+    }
+    int rc = GF2_OK;
+    // ---- pre-additions, level by level
+    for (int lv = 0; lv < depth && rc == GF2_OK; ++lv) {
+        for (int side = 0; side < 2 && rc == GF2_OK; ++side) {
+            CombineArgs c{};
+            const bool isA = side == 0;
+            const int64_t R = isA ? M[lv + 1] : L[lv + 1];
+            const int64_t W = isA ? Lw[lv + 1] : Nw[lv + 1];
+            if (lv == 0) {
+                c.src = isA ? A0.data : B0.data;
+                c.src_pitch = isA ? A0.pitch : B0.pitch;
+                c.src_stride = 0;
+            } else {
+                c.src = ws + (isA ? offA[lv] : offB[lv]);
+                c.src_pitch = isA ? Lw[lv] : Nw[lv];
+                c.src_stride = (isA ? M[lv] : L[lv]) * c.src_pitch;
+            }
+            c.src_off[0] = 0;
+            c.src_off[1] = W;
+            c.src_off[2] = R * c.src_pitch;
+            c.src_off[3] = R * c.src_pitch + W;
+            c.dst = ws + (isA ? offA[lv + 1] : offB[lv + 1]);
+            c.dst_pitch = W;
+            c.dst_stride = 7 * R * W;
+            for (int q = 0; q < 7; ++q) {
+                c.dst_off[q] = q * R * W;
+                c.mask[q] = isA ? kSA[q] : kSB[q];
+            }
+            c.nq = 7;
+            c.R = R;
+            c.W = W;
+            c.nprob = P[lv];
+            c.accumulate = 0;
+            rc = launch_combine(c, s);
+        }
+    }
+    // ---- all 7^d leaf products in one batched M4RM launch
+    if (rc == GF2_OK) {
+        M4rmBatch mb{ws + offA[depth], Lw[depth], M[depth] * Lw[depth],
+                     ws + offB[depth], Nw[depth], L[depth] * Nw[depth],
+                     ws + offC[depth], Nw[depth], M[depth] * Nw[depth],
+                     M[depth], L[depth], N[depth], P[depth], 0};
+        rc = launch_m4rm(mb, s);
+    }
+    // ---- post-combination, deepest level first
+    for (int lv = depth - 1; lv >= 0 && rc == GF2_OK; --lv) {
+        CombineArgs c{};
+        const int64_t R = M[lv + 1], W = Nw[lv + 1];
+        c.src = ws + offC[lv + 1];
+        c.src_pitch = W;
+        c.src_stride = 7 * R * W;
+        for (int i = 0; i < 7; ++i) c.src_off[i] = i * R * W;
+        if (lv == 0) {
+            c.dst = C0.data;
+            c.dst_pitch = C0.pitch;
+            c.dst_stride = 0;
+        } else {
+            c.dst = ws + offC[lv];
+            c.dst_pitch = Nw[lv];
+            c.dst_stride = M[lv] * Nw[lv];
+        }
+        c.dst_off[0] = 0;
+        c.dst_off[1] = W;
+        c.dst_off[2] = R * c.dst_pitch;
+        c.dst_off[3] = R * c.dst_pitch + W;
+        for (int q = 0; q < 4; ++q) c.mask[q] = kSC[q];
+        c.nq = 4;
+        c.R = R;
+        c.W = W;
+        c.nprob = P[lv];
+        c.accumulate = lv == 0 ? accumulate : 0;
+        rc = launch_combine(c, s);
+    }
+    cudaFreeAsync(ws, s);
+    return rc;
+}
+
+}  // namespace
+
+// strassen.py:66-84
+void peel_split(int64_t m, int64_t l, int64_t n, int64_t cutoff, int64_t out[4]) {
+    out[0] = out[1] = out[2] = out[3] = 0;
+    auto ok = [&](int d) {
+        int64_t unit = (int64_t)kWordBits << d;
+        return (m / unit) * kWordBits >= cutoff && (l / unit) * kWordBits >= cutoff &&
+               (n / unit) * kWordBits >= cutoff;
+    };
+    if (m < 1 || l < 1 || n < 1 || !ok(1)) return;
+    int depth = 1;
+    while (depth < 20 && ok(depth + 1)) ++depth;
+    int64_t unit = (int64_t)kWordBits << depth;
+    out[0] = (m / unit) * unit;
+    out[1] = (l / unit) * unit;
+    out[2] = (n / unit) * unit;
+    out[3] = depth;
+}
+
+int m4rm_mul(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accumulate, cudaStream_t s) {
+    return m4rm_view(c, a, b, accumulate, s);
+}
+
+// strassen.py:257-282 dispatch (+ peel_fixup strassen.py:219-249).
+int strassen_mul(const gf2_view &C, const gf2_view &A, const gf2_view &B, int64_t cutoff, int accumulate,
+                 cudaStream_t s) {
+    const int64_t m = A.nrows, l = A.ncols, n = B.ncols;
+    if (!m || !n) return GF2_OK;
+    if (!l) return accumulate ? GF2_OK : launch_ewise(C, nullptr, nullptr, 0, s);
+    // n < 64: the reference switches to mul_cubic (strassen.py:268-269); the
+    // product is the same, and the M4RM kernel handles a single-word tile.
+    const int64_t mn = m < l ? (m < n ? m : n) : (l < n ? l : n);
+    if (n < kWordBits || mn <= cutoff) return m4rm_view(C, A, B, accumulate, s);
+    int64_t ps[4];
+    peel_split(m, l, n, cutoff, ps);
+    if (ps[3] == 0) return m4rm_view(C, A, B, accumulate, s);
+    const int64_t m2 = ps[0], l2 = ps[1], n2 = ps[2];
+    GF2_TRY(strassen_core(sub_view(C, 0, 0, m2, n2), sub_view(A, 0, 0, m2, l2), sub_view(B, 0, 0, l2, n2),
+                          (int)ps[3], accumulate, s));
+    // peel_fixup: inner remainder (accumulate), bottom rows, right columns
+    if (l2 < l)
+        GF2_TRY(m4rm_view(sub_view(C, 0, 0, m2, n2), sub_view(A, 0, l2, m2, l - l2), sub_view(B, l2, 0, l - l2, n2),
+                          1, s));
+    if (m2 < m)
+        GF2_TRY(m4rm_view(sub_view(C, m2, 0, m - m2, n), sub_view(A, m2, 0, m - m2, l), B, accumulate, s));
+    if (n2 < n)
+        GF2_TRY(m4rm_view(sub_view(C, 0, n2, m2, n - n2), sub_view(A, 0, 0, m2, l), sub_view(B, 0, n2, l, n - n2),
+                          accumulate, s));
+    return GF2_OK;
+}
+
+}  // namespace gf2

@@ -1,0 +1,88 @@
+"""Method of the Four Russians on B200 -- the reference's M4RM entry points
+(m4rm.py:124-155) with the same signatures, validation and errors, backed by
+the sm_100a kernel in csrc/gf2_m4rm.cu.
+
+k, t and b_s are the reference's CPU knobs (table width, tables per fused
+update, cache row block). They are validated exactly as the reference does
+(StripeSpec, m4rm.py:28-42); the device kernel fixes its own geometry
+(8-bit Gray tables, 4 per 32-row half stage, register-resident C tiles),
+which changes nothing in the result: the product is exact.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from . import _lib
+from .core import BitMatrix, Mat, _check_cuda_dev, _stream, create
+from .errors import DimensionError, ParameterError
+
+MAX_K = 16
+
+
+@dataclass(frozen=True)
+class StripeSpec:
+    """m4rm.py:28-42 -- validated stripe parameters."""
+
+    k: int
+    t: int = 1
+    b_s: int = 1
+
+    def __post_init__(self):
+        if not 1 <= self.k <= MAX_K:
+            raise ParameterError(f"k={self.k} outside 1..{MAX_K}")
+        if not 1 <= self.t <= 8:
+            raise ParameterError(f"t={self.t} outside 1..8")
+        if self.b_s < 1:
+            raise ParameterError(f"block size {self.b_s} < 1")
+
+
+def _validate(a: Mat, b: Mat, k: int, t: int, b_s: int) -> StripeSpec:
+    """m4rm.py:69-74"""
+    if a.ncols != b.nrows:
+        raise DimensionError(
+            f"inner dimensions {a.ncols} and {b.nrows} differ")
+    return StripeSpec(k, t, b_s)
+
+
+def _mul_into(c: Mat, a: Mat, b: Mat, k: int, accumulate: bool) -> None:
+    _check_cuda_dev(c, a, b)
+    _lib.check(_lib.lib_cuda().gf2_m4rm(c._view(), a._view(), b._view(),
+                                        int(k), int(accumulate), _stream()))
+
+
+def mul_m4rm(a: Mat, b: Mat, k: int) -> BitMatrix:
+    """m4rm.py:124-129 -- basic Four-Russians product."""
+    _validate(a, b, k, 1, 1)
+    c = create(a.nrows, b.ncols, a.device)
+    _mul_into(c, a, b, k, False)
+    return c
+
+
+def mul_m4rm_blocked(a: Mat, b: Mat, k: int, b_s: int) -> BitMatrix:
+    """m4rm.py:132-137"""
+    _validate(a, b, k, 1, b_s)
+    c = create(a.nrows, b.ncols, a.device)
+    _mul_into(c, a, b, k, False)
+    return c
+
+
+def mul_m4rm_multitable(a: Mat, b: Mat, k: int, t: int,
+                        b_s: int) -> BitMatrix:
+    """m4rm.py:140-147"""
+    _validate(a, b, k, t, b_s)
+    c = create(a.nrows, b.ncols, a.device)
+    _mul_into(c, a, b, k, False)
+    return c
+
+
+def mul_m4rm_into(c: BitMatrix, a: Mat, b: Mat, k: int,
+                  b_s: int | None = None, t: int = 1) -> None:
+    """m4rm.py:150-155 -- c += a @ b into an owned c."""
+    b_s = max(a.nrows, 1) if b_s is None else b_s
+    _validate(a, b, k, t, b_s)
+    assert isinstance(c, BitMatrix), "M4RM writes into owned C only"
+    if c.nrows != a.nrows or c.ncols != b.ncols:
+        raise DimensionError(
+            f"target {c.nrows}x{c.ncols} != product {a.nrows}x{b.ncols}")
+    _mul_into(c, a, b, k, True)

@@ -1,0 +1,87 @@
+"""Multi-GPU C += A.B on one 8xB200 box (north_star (e)).
+
+One process per GPU (torch.distributed, NCCL over NVLink 5 / NVSwitch).
+C is sharded by row blocks and A is row-sharded the same way, so every rank
+computes C_p (+)= A_p . B locally and NO reduction is needed (XOR
+accumulation is shard-local). B lives on rank `src` and is broadcast once,
+in K-panels: panel i+1 is on the wire (NCCL's stream) while panel i is
+multiplied (this rank's stream), so the broadcast hides behind compute.
+Bit-exactness across world sizes is automatic: the arithmetic is exact.
+
+The plan/pipeline logic is backend-agnostic (tests drive it with gloo on
+CPU tensors and an injected local multiply); `mul_sharded` binds it to the
+device path.
+"""
+
+from __future__ import annotations
+
+from typing import Callable, Sequence
+
+_WORD = 64
+
+
+def shard_rows(m: int, world: int, rank: int, align: int = _WORD):
+    """Row range [r0, r1) of rank `rank`: equal blocks rounded up to
+    `align` rows (so Strassen quadrants stay aligned), last rank short."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world {world}")
+    per = -(-m // world)
+    per = -(-per // align) * align if m >= align * world else per
+    r0 = min(m, rank * per)
+    r1 = min(m, r0 + per)
+    return r0, r1
+
+
+def k_panels(l: int, npanels: int) -> list[tuple[int, int]]:
+    """Split the inner dimension into word-aligned panels [k0, k1)."""
+    if l == 0:
+        return []
+    npanels = max(1, min(npanels, -(-l // _WORD)))
+    words = -(-l // _WORD)
+    per = -(-words // npanels)
+    out = []
+    for p in range(npanels):
+        k0, k1 = p * per * _WORD, min(l, (p + 1) * per * _WORD)
+        if k0 < k1:
+            out.append((k0, k1))
+    return out
+
+
+def pipelined_broadcast(b_rows, panels: Sequence[tuple[int, int]],
+                        local_addmul: Callable[[int, int], None],
+                        src: int = 0, group=None) -> None:
+    """Broadcast row panels of `b_rows` (a [l, pitch] tensor; rows = B's
+    rows) from `src` asynchronously, and run local_addmul(k0, k1) for each
+    panel as soon as it has landed."""
+    import torch.distributed as dist
+    works = [dist.broadcast(b_rows[k0:k1], src=src, group=group,
+                            async_op=True) for k0, k1 in panels]
+    for (k0, k1), w in zip(panels, works):
+        w.wait()
+        local_addmul(k0, k1)
+
+
+def mul_sharded(a_shard, b, params=None, src: int = 0, group=None,
+                npanels: int = 4, c=None):
+    """C_p (+)= A_p . B on this rank. `b` is a BitMatrix of B's full shape
+    on every rank; its contents matter only on `src`. If `c` is given the
+    product is accumulated into it (addmul), else a fresh C_p is returned."""
+    from .core import create, window
+    from .strassen import addmul
+
+    m, l, n = a_shard.nrows, a_shard.ncols, b.ncols
+    if c is None:
+        c = create(m, n, a_shard.device)
+    panels = k_panels(l, npanels)
+
+    def local(k0: int, k1: int) -> None:
+        addmul(c, window(a_shard, 0, k0, m, k1 - k0),
+               window(b, k0, 0, k1 - k0, n), params)
+
+    if not panels:
+        return c
+    pipelined_broadcast(b.storage, panels, local, src=src, group=group)
+    return c
+
+
+__all__ = ["shard_rows", "k_panels", "pipelined_broadcast", "mul_sharded"]

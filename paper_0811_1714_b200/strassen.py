@@ -1,0 +1,110 @@
+"""Strassen-Winograd with peeling on B200 -- the reference's entry points
+(strassen.py:27-84, 257-282) with the same signatures and validation.
+
+The recursion itself runs natively (csrc/gf2_strassen.cu): the same peel
+rule and the same depth as the reference for the given cutoff, but each
+recursion level is one batched device launch (all 7^s sub-products at
+once) instead of a depth-first walk with two scratch quadrants.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import NamedTuple
+
+from . import _lib
+from .core import BitMatrix, Mat, _check_cuda_dev, _stream, create
+from .errors import DimensionError, ParameterError
+
+_WORD = 64
+
+# Crossover chosen for the B200: below it a single M4RM
+# launch fills the GPU better than a level of 7 sub-products plus 15 adds.
+GPU_CUTOFF = 4096
+
+
+@dataclass
+class MulParams:
+    """strassen.py:27-56 -- same fields, defaults and invariants.
+
+    On the device, `cutoff` sets the recursion depth exactly as in the
+    reference (peel_split); `k`, `t`, `b_s`, `l1_bytes`, `l2_bytes` are
+    validated and recorded (the kernel picks its own tiling).
+    """
+
+    cutoff: int = 2048
+    b_s: int | None = None
+    k: int = 0
+    t: int = 8
+    l1_bytes: int = 32768
+    l2_bytes: int = 1 << 20
+
+    def __post_init__(self):
+        if self.b_s is None:
+            self.b_s = max(self.cutoff // 2, 1)
+        if self.cutoff < 64:
+            raise ParameterError(f"cutoff {self.cutoff} < 64")
+        if not 1 <= self.t <= 8:
+            raise ParameterError(f"t={self.t} outside 1..8")
+        if not 0 <= self.k <= 16:
+            raise ParameterError(f"k={self.k} outside 0..16")
+        if not 1 <= self.b_s <= self.cutoff:
+            raise ParameterError(
+                f"block size {self.b_s} outside 1..cutoff={self.cutoff}")
+
+
+class PeelSplit(NamedTuple):
+    m: int
+    l: int
+    n: int
+    depth: int
+
+
+def peel_split(m: int, l: int, n: int, cutoff: int) -> PeelSplit:
+    """strassen.py:66-84 (evaluated by the native library)."""
+    out = (ctypes.c_int64 * 4)()
+    _lib.check(_lib.load().gf2_peel_split(m, l, n, cutoff, out))
+    return PeelSplit(*(int(x) for x in out))
+
+
+def default_params() -> MulParams:
+    """Device defaults (the reference derives its from CPU cache sizes,
+    tuning.py:47-65): recursion above GPU_CUTOFF, M4RM below."""
+    return MulParams(cutoff=GPU_CUTOFF, k=8, t=8)
+
+
+def _strassen(c: Mat, a: Mat, b: Mat, params: MulParams,
+              accumulate: bool) -> None:
+    _check_cuda_dev(c, a, b)
+    _lib.check(_lib.lib_cuda().gf2_strassen(
+        c._view(), a._view(), b._view(), int(params.cutoff), int(params.k),
+        int(accumulate), _stream()))
+
+
+def mul_strassen(a: Mat, b: Mat, params: MulParams | None = None) -> BitMatrix:
+    """strassen.py:257-282 -- full dispatch: recursion, then M4RM."""
+    if a.ncols != b.nrows:
+        raise DimensionError(
+            f"inner dimensions {a.ncols} and {b.nrows} differ")
+    if params is None:
+        params = default_params()
+    c = create(a.nrows, b.ncols, a.device)
+    if a.nrows and b.ncols and a.ncols:
+        _strassen(c, a, b, params, False)
+    return c
+
+
+def addmul(c: Mat, a: Mat, b: Mat, params: MulParams | None = None) -> None:
+    """C += A.B at Strassen scale (cfg4/cfg5 addmul). The reference spells
+    this add_into(C, C, mul_strassen(A, B)); here the final
+    Winograd combination XORs straight into C (a window is fine)."""
+    if a.ncols != b.nrows:
+        raise DimensionError(
+            f"inner dimensions {a.ncols} and {b.nrows} differ")
+    if c.nrows != a.nrows or c.ncols != b.ncols:
+        raise DimensionError(
+            f"target {c.nrows}x{c.ncols} != product {a.nrows}x{b.ncols}")
+    if params is None:
+        params = default_params()
+    _strassen(c, a, b, params, True)

@@ -1,0 +1,66 @@
+"""Host-side logic mirroring the reference: parameter bundles, peel rule,
+shard / panel plans. CPU only."""
+
+import numpy as np
+import pytest
+
+from paper_0811_1714_b200 import (MulParams, ParameterError, StripeSpec,
+                                  default_params)
+from paper_0811_1714_b200.sharded import k_panels, shard_rows
+
+
+def test_mulparams_mirror():
+    # test_strassen.py:21-35
+    assert MulParams(cutoff=128).b_s == 64
+    for kw in [dict(cutoff=32), dict(cutoff=128, t=9),
+               dict(cutoff=128, b_s=256), dict(cutoff=128, k=17)]:
+        with pytest.raises(ParameterError):
+            MulParams(**kw)
+    p = default_params()
+    assert p.cutoff >= 64 and 1 <= p.b_s <= p.cutoff
+
+
+def test_stripespec_mirror():
+    # test_m4rm.py:21-34
+    s = StripeSpec(k=6, t=8, b_s=256)
+    assert (s.k, s.t, s.b_s) == (6, 8, 256)
+    for kw in [dict(k=0), dict(k=17), dict(k=4, t=9), dict(k=4, t=1, b_s=0)]:
+        with pytest.raises(ParameterError):
+            StripeSpec(**kw)
+
+
+def test_peel_split_properties():
+    # test_strassen.py:50-63
+    from paper_0811_1714_b200 import peel_split
+    rng = np.random.default_rng(1)
+    for _ in range(200):
+        m, l, n = (int(x) for x in rng.integers(1, 5000, 3))
+        ps = peel_split(m, l, n, 128)
+        if ps.depth == 0:
+            continue
+        unit = 64 << ps.depth
+        for x, x0 in [(ps.m, m), (ps.l, l), (ps.n, n)]:
+            assert x % unit == 0 and x <= x0 < x + unit
+            assert (x >> ps.depth) >= 128 and (x >> ps.depth) % 64 == 0
+
+
+@pytest.mark.parametrize("m,world", [(16384, 1), (16384, 2), (16384, 8),
+                                     (65536, 8), (10000, 3), (100, 8),
+                                     (7, 4)])
+def test_shard_rows_partition(m, world):
+    spans = [shard_rows(m, world, r) for r in range(world)]
+    assert spans[0][0] == 0 and spans[-1][1] == m
+    for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+        assert a1 == b0 and a0 <= a1
+    if m >= 64 * world:
+        assert all(r0 % 64 == 0 for r0, _ in spans)
+
+
+def test_k_panels():
+    assert k_panels(0, 4) == []
+    for l, p in [(16384, 4), (7001, 3), (64, 8), (65, 2), (1, 1)]:
+        ps = k_panels(l, p)
+        assert ps[0][0] == 0 and ps[-1][1] == l
+        assert all(k0 % 64 == 0 for k0, _ in ps)
+        for (a0, a1), (b0, b1) in zip(ps, ps[1:]):
+            assert a1 == b0
