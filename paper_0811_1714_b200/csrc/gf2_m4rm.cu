@@ -38,18 +38,20 @@ namespace gf2 {
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;   // 16 warps = 64 quarter-warp row groups
+constexpr int kRowGroups = kThreads / 8;
 constexpr int kTables = 4;      // 8-bit tables per half stage (32 rows of B)
 constexpr int kTabRows = 256;   // 2^8 slots
 constexpr int kTileWords = 16;  // 1024 columns per C tile
 constexpr int kRowBytes = kTileWords * 8;
 constexpr int kTableBytes = kTabRows * kRowBytes;     // 32 KiB
-constexpr int kStageRows = 64;                         // rows of B per stage
-constexpr int kBStageBytes = kStageRows * kRowBytes;  // 8 KiB
+constexpr int kStageWords = 2;                         // A words per stage
+constexpr int kStageRows = 64 * kStageWords;           // rows of B per stage
+constexpr int kBStageBytes = kStageRows * kRowBytes;  // 16 KiB
 
 template <int RPT>
 constexpr int smem_bytes() {
-    return kTables * kTableBytes + 2 * kBStageBytes + 2 * (32 * RPT) * 8;
+    return kTables * kTableBytes + 2 * kBStageBytes + 2 * (kRowGroups * RPT) * 8 * kStageWords;
 }
 
 struct KArgs {
@@ -61,15 +63,20 @@ struct KArgs {
     int64_t pc, sc;
     int64_t m, l, n;
     int64_t Wl, Wn;
-    int64_t kws;  // A words per split
+    int64_t kws;  // A words per split (even unless it is the whole row)
     int nsplit;
     int mode;  // 0 store, 1 xor, 2 atomic xor
 };
 
-__device__ __forceinline__ void cp_async8(uint32_t saddr, const void *g, bool pred) {
-    int sz = pred ? 8 : 0;
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(g), "r"(sz)
-                 : "memory");
+// cp.async with zero-fill: copies `bytes` (0..CP) of CP and zero-fills the rest.
+template <int CP>
+__device__ __forceinline__ void cp_async(uint32_t saddr, const void *g, int bytes) {
+    if (CP == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(g), "r"(bytes)
+                     : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(g), "r"(bytes)
+                     : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
@@ -80,20 +87,26 @@ __device__ __forceinline__ void sts128(uint32_t addr, u64 a, u64 b) {
 __device__ __forceinline__ void lds128(uint32_t addr, u64 &a, u64 &b) {
     asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];\n" : "=l"(a), "=l"(b) : "r"(addr));
 }
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(addr));
+    return v;
+}
 
-template <int RPT>
+// C tile: BM = 64*RPT rows x 1024 columns, in registers. ALIGN16: operands
+// allow 16-byte cp.async (base and pitch 16-byte aligned).
+template <int RPT, bool ALIGN16>
 __global__ void __launch_bounds__(kThreads, 1) k_m4rm(KArgs p) {
-    constexpr int BM = 32 * RPT;
+    constexpr int BM = kRowGroups * RPT;
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t s_tab = (uint32_t)__cvta_generic_to_shared(smem);
     const uint32_t s_bst = s_tab + kTables * kTableBytes;
     const uint32_t s_ast = s_bst + 2 * kBStageBytes;
-    const u64 *a_st = reinterpret_cast<const u64 *>(smem + kTables * kTableBytes + 2 * kBStageBytes);
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    const int s = lane & 7;                    // 128-bit column slice
-    const int rg = (tid >> 5) * 4 + (lane >> 3);  // row group 0..31
+    const int s = lane & 7;                       // 128-bit column slice
+    const int rg = (tid >> 5) * 4 + (lane >> 3);  // row group 0..63
 
     const int64_t prob = blockIdx.z / p.nsplit;
     const int split = blockIdx.z % p.nsplit;
@@ -112,25 +125,49 @@ __global__ void __launch_bounds__(kThreads, 1) k_m4rm(KArgs p) {
     const u64 bm0 = (wj0 == p.Wn - 1) ? tail_mask(p.n) : ~0ULL;
     const u64 bm1 = (wj0 + 1 == p.Wn - 1) ? tail_mask(p.n) : ~0ULL;
 
+    // stage = A words [kw, kw+2) of BM rows and the 128 matching rows of B
     auto load_stage = [&](int64_t kw, int buf) {
-        // B panel: 64 rows x 16 words
+        const uint32_t bdst = s_bst + buf * kBStageBytes;
+        if (ALIGN16) {
 #pragma unroll
-        for (int i = 0; i < (kStageRows * kTileWords) / kThreads; ++i) {
-            int e = tid + kThreads * i;
-            int r = e >> 4, wd = e & 15;
-            int64_t brow = kw * 64 + r;
-            bool ok = (brow < p.l) && (col_w0 + wd < p.Wn);
-            const u64 *src = ok ? (B + brow * p.pb + col_w0 + wd) : B;
-            cp_async8(s_bst + buf * kBStageBytes + r * kRowBytes + wd * 8, src, ok);
-        }
-        // A column words for the BM rows
+            for (int i = 0; i < (kStageRows * kTileWords / 2) / kThreads; ++i) {
+                const int e = tid + kThreads * i;
+                const int r = e >> 3, c2 = (e & 7) * 2;
+                const int64_t brow = kw * 64 + r;
+                const int64_t wv = p.Wn - (col_w0 + c2);
+                const int bytes = (brow < p.l) ? (wv >= 2 ? 16 : (wv == 1 ? 8 : 0)) : 0;
+                const u64 *src = bytes ? (B + brow * p.pb + col_w0 + c2) : B;
+                cp_async<16>(bdst + r * kRowBytes + c2 * 8, src, bytes);
+            }
 #pragma unroll
-        for (int i = 0; i < (BM + kThreads - 1) / kThreads; ++i) {
-            int r = tid + kThreads * i;
-            if (r < BM) {
-                bool ok = row0 + r < p.m;
-                const u64 *src = ok ? (A + (row0 + r) * p.pa + kw) : A;
-                cp_async8(s_ast + (buf * BM + r) * 8, src, ok);
+            for (int i = 0; i < (BM + kThreads - 1) / kThreads; ++i) {
+                const int r = tid + kThreads * i;
+                if (r < BM) {
+                    const int64_t wv = kw1 - kw;
+                    const int bytes = (row0 + r < p.m) ? (wv >= 2 ? 16 : 8) : 0;
+                    const u64 *src = bytes ? (A + (row0 + r) * p.pa + kw) : A;
+                    cp_async<16>(s_ast + (buf * BM + r) * 16, src, bytes);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < (kStageRows * kTileWords) / kThreads; ++i) {
+                const int e = tid + kThreads * i;
+                const int r = e >> 4, wd = e & 15;
+                const int64_t brow = kw * 64 + r;
+                const bool ok = (brow < p.l) && (col_w0 + wd < p.Wn);
+                const u64 *src = ok ? (B + brow * p.pb + col_w0 + wd) : B;
+                cp_async<8>(bdst + r * kRowBytes + wd * 8, src, ok ? 8 : 0);
+            }
+#pragma unroll
+            for (int i = 0; i < (2 * BM + kThreads - 1) / kThreads; ++i) {
+                const int e = tid + kThreads * i;
+                if (e < 2 * BM) {
+                    const int r = e >> 1, wd = e & 1;
+                    const bool ok = (row0 + r < p.m) && (kw + wd < kw1);
+                    const u64 *src = ok ? (A + (row0 + r) * p.pa + kw + wd) : A;
+                    cp_async<8>(s_ast + (buf * BM + r) * 16 + wd * 8, src, ok ? 8 : 0);
+                }
             }
         }
         cp_async_commit();
@@ -140,53 +177,57 @@ __global__ void __launch_bounds__(kThreads, 1) k_m4rm(KArgs p) {
 #pragma unroll
     for (int i = 0; i < RPT; ++i) acc[i][0] = acc[i][1] = 0ULL;
 
-    // table-build role: table tj, slots [r0*32, r0*32+32), slice s
-    const int tj = rg >> 3, r0 = rg & 7;
+    // table-build role: table tj, slots [r0*16, r0*16+16), slice s
+    const int tj = rg >> 4, r0 = rg & 15;
 
     if (kw0 < kw1) load_stage(kw0, 0);
-    for (int64_t kw = kw0; kw < kw1; ++kw) {
-        const int buf = (int)((kw - kw0) & 1);
+    int buf = 0;
+    for (int64_t kw = kw0; kw < kw1; kw += kStageWords, buf ^= 1) {
         cp_async_wait_all();
-        __syncthreads();  // stage kw visible; previous lookups finished
-        if (kw + 1 < kw1) load_stage(kw + 1, buf ^ 1);
-        const u64 amask = (kw == p.Wl - 1) ? atm : ~0ULL;
-
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            if (h == 1) __syncthreads();  // lookups of half 0 done before rebuild
-            // ---- build table tj from B rows 32h + 8tj + (0..7), slice s
+        __syncthreads();  // stage visible; previous lookups finished
+        if (kw + kStageWords < kw1) load_stage(kw + kStageWords, buf ^ 1);
+        const int nhalf = (kw + 1 < kw1) ? 4 : 2;
+        for (int hs = 0; hs < nhalf; ++hs) {
+            if (hs) __syncthreads();  // lookups of the previous half done before rebuild
+            // ---- build table tj from B rows 32hs + 8tj + (0..7), slice s
             {
-                u64 x0[8], x1[8];
-                const uint32_t srow = s_bst + buf * kBStageBytes + (32 * h + 8 * tj) * kRowBytes + s * 16;
+                const uint32_t srow = s_bst + buf * kBStageBytes + (32 * hs + 8 * tj) * kRowBytes + s * 16;
+                u64 c0 = 0, c1 = 0, y0, y1;
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    lds128(srow + i * kRowBytes, x0[i], x1[i]);
+                for (int i = 0; i < 4; ++i) {  // slot bits 7..4 <-> source rows 0..3
+                    lds128(srow + i * kRowBytes, y0, y1);
+                    const u64 sel = (r0 & (8 >> i)) ? ~0ULL : 0ULL;
+                    c0 ^= y0 & bm0 & sel;
+                    c1 ^= y1 & bm1 & sel;
+                }
+                u64 x0[4], x1[4];  // slot bits 3..0 <-> source rows 4..7
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    lds128(srow + (4 + i) * kRowBytes, x0[i], x1[i]);
                     x0[i] &= bm0;
                     x1[i] &= bm1;
                 }
-                u64 c0 = 0, c1 = 0;
-                if (r0 & 4) { c0 ^= x0[0]; c1 ^= x1[0]; }
-                if (r0 & 2) { c0 ^= x0[1]; c1 ^= x1[1]; }
-                if (r0 & 1) { c0 ^= x0[2]; c1 ^= x1[2]; }
-                const uint32_t tbase = s_tab + tj * kTableBytes + (r0 * 32) * kRowBytes + s * 16;
+                const uint32_t tbase = s_tab + tj * kTableBytes + (r0 * 16) * kRowBytes + s * 16;
                 sts128(tbase, c0, c1);
 #pragma unroll
-                for (int i = 1; i < 32; ++i) {
-                    const int b = (i & 1) ? 0 : (i & 2) ? 1 : (i & 4) ? 2 : (i & 8) ? 3 : 4;  // flipped Gray bit
+                for (int i = 1; i < 16; ++i) {
+                    const int b = (i & 1) ? 0 : (i & 2) ? 1 : (i & 4) ? 2 : 3;  // flipped Gray bit
                     const int g = i ^ (i >> 1);
-                    c0 ^= x0[7 - b];                  // slot bit b <-> source row 7-b
-                    c1 ^= x1[7 - b];
+                    c0 ^= x0[3 - b];  // slot bit b <-> source row 7-b
+                    c1 ^= x1[3 - b];
                     sts128(tbase + g * kRowBytes, c0, c1);
                 }
             }
             __syncthreads();
-            // ---- lookups
+            // ---- lookups: A half-word hs of the stage (word hs/2, high half first)
+            const int64_t wcur = kw + (hs >> 1);
+            const uint32_t amask = (uint32_t)(((wcur == p.Wl - 1) ? atm : ~0ULL) >> ((hs & 1) ? 0 : 32));
+            const uint32_t aoff = s_ast + buf * BM * 16 + (hs >> 1) * 8 + ((hs & 1) ? 0 : 4);
+            const uint32_t base = s_tab + s * 16;
 #pragma unroll
             for (int i = 0; i < RPT; ++i) {
-                u64 a = a_st[buf * BM + i * 32 + rg] & amask;
-                uint32_t hw = (h == 0) ? (uint32_t)(a >> 32) : (uint32_t)a;
+                const uint32_t hw = lds32(aoff + (i * kRowGroups + rg) * 16) & amask;
                 u64 v0, v1, w0, w1;
-                const uint32_t base = s_tab + s * 16;
                 lds128(base + 0 * kTableBytes + ((hw >> 24) & 0xFF) * kRowBytes, v0, v1);
                 lds128(base + 1 * kTableBytes + ((hw >> 16) & 0xFF) * kRowBytes, w0, w1);
                 acc[i][0] ^= v0 ^ w0;
@@ -203,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_m4rm(KArgs p) {
     const u64 ctm = tail_mask(p.n);
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-        const int64_t row = row0 + i * 32 + rg;
+        const int64_t row = row0 + i * kRowGroups + rg;
         if (row >= p.m) continue;
         u64 *crow = C + row * p.pc;
 #pragma unroll
@@ -224,17 +265,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_m4rm(KArgs p) {
     }
 }
 
-template <int RPT>
+template <int RPT, bool A16>
 int launch_rpt(const KArgs &ka, int64_t col_tiles, int64_t row_tiles, int64_t zdim, cudaStream_t s) {
     static bool configured = false;
     constexpr int sm = smem_bytes<RPT>();
     if (!configured) {
-        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_m4rm<RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_m4rm<RPT, A16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
                            "cudaFuncSetAttribute(k_m4rm)"));
         configured = true;
     }
     dim3 grid((unsigned)col_tiles, (unsigned)row_tiles, (unsigned)zdim);
-    k_m4rm<RPT><<<grid, kThreads, sm, s>>>(ka);
+    k_m4rm<RPT, A16><<<grid, kThreads, sm, s>>>(ka);
     note_launch();
     return check_cuda(cudaGetLastError(), "k_m4rm launch");
 }
@@ -313,10 +354,10 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     const int64_t col_tiles = (Wn + kTileWords - 1) / kTileWords;
     const int64_t want = g_num_sms;  // one CTA per SM is resident (smem-bound)
     int rpt = 16;
-    int64_t row_tiles = (b.m + 32 * rpt - 1) / (32 * rpt);
+    int64_t row_tiles = (b.m + kRowGroups * rpt - 1) / (kRowGroups * rpt);
     while (rpt > 4 && row_tiles * col_tiles * b.nprob < want) {
         rpt /= 2;
-        row_tiles = (b.m + 32 * rpt - 1) / (32 * rpt);
+        row_tiles = (b.m + kRowGroups * rpt - 1) / (kRowGroups * rpt);
     }
     const int64_t tiles = row_tiles * col_tiles * b.nprob;
     int nsplit = 1;
@@ -326,6 +367,7 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
         nsplit = (int)ns;
     }
     int64_t kws = (Wl + nsplit - 1) / nsplit;
+    kws = (kws + kStageWords - 1) / kStageWords * kStageWords;  // splits start on a stage
     nsplit = (int)((Wl + kws - 1) / kws);
     if ((int64_t)nsplit * b.nprob > 65535 || row_tiles > 65535)
         return set_error(GF2_ERR_PARAMETER, "m4rm grid too large");
@@ -345,13 +387,18 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
         tl.bitops = (double)b.m * (double)b.l * (double)b.n * (double)b.nprob;
         cudaEventRecord(tl.a, s);
     }
+    const bool a16 = ((uintptr_t)b.A % 16 == 0) && ((uintptr_t)b.B % 16 == 0) && (b.pa % 2 == 0) &&
+                     (b.pb % 2 == 0) && (b.nprob == 1 || (b.sa % 2 == 0 && b.sb % 2 == 0));
     int rc;
     if (rpt == 16)
-        rc = launch_rpt<16>(ka, col_tiles, row_tiles, z, s);
+        rc = a16 ? launch_rpt<16, true>(ka, col_tiles, row_tiles, z, s)
+                 : launch_rpt<16, false>(ka, col_tiles, row_tiles, z, s);
     else if (rpt == 8)
-        rc = launch_rpt<8>(ka, col_tiles, row_tiles, z, s);
+        rc = a16 ? launch_rpt<8, true>(ka, col_tiles, row_tiles, z, s)
+                 : launch_rpt<8, false>(ka, col_tiles, row_tiles, z, s);
     else
-        rc = launch_rpt<4>(ka, col_tiles, row_tiles, z, s);
+        rc = a16 ? launch_rpt<4, true>(ka, col_tiles, row_tiles, z, s)
+                 : launch_rpt<4, false>(ka, col_tiles, row_tiles, z, s);
     if (g_timing) {
         cudaEventRecord(tl.b, s);
         g_timed.push_back(tl);
