@@ -44,6 +44,8 @@ def parse():
     p.add_argument("--cutoff", type=int, default=0,
                    help="Strassen cutoff (0 = device default)")
     p.add_argument("--npanels", type=int, default=4)
+    p.add_argument("--engine", default="m4rm", choices=["m4rm", "tc-i8", "tc-f8"],
+                   help="product engine (results are identical)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-verify", action="store_true")
@@ -218,6 +220,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
+    g.set_engine(args.engine)
     w = dict(WORKLOAD)
     if args.size:
         w.update(m=args.size, l=args.size, n=args.size)

@@ -118,6 +118,11 @@ int64_t gf2_launch_count(void);
  * and returns the summed kernel milliseconds, the algorithmic bit-ops
  * (m*l*n per product) those launches computed, and the launch count. */
 int gf2_timer_enable(int on);
+/* Engine for every product (M4RM calls and Strassen leaves), process-wide:
+ * 0 = M4RM shared-memory Gray tables (default), 1 = tcgen05 kind::i8,
+ * 2 = tcgen05 kind::f8f6f4 (e4m3 0/1). Results are identical. */
+int gf2_set_engine(int engine);
+int gf2_get_engine(void);
 int gf2_timer_read(double *kernel_ms, double *bitops, int64_t *launches);
 
 #ifdef __cplusplus

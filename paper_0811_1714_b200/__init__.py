@@ -8,7 +8,8 @@ hand-written sm_100a kernels in libgf2b200.so. No CPU fallback exists: if
 the library or the GPU is missing, operations raise NativeUnavailable.
 """
 
-from ._lib import DeviceError, NativeUnavailable, launch_count
+from ._lib import (DeviceError, NativeUnavailable, get_engine, launch_count,
+                   set_engine)
 from .core import (BitMatrix, HostMatrix, MatrixWindow, add, add_into,
                    bernoulli, copy_into, copy_out, create, equal,
                    first_difference, from_dense, from_host, from_numpy,
@@ -29,8 +30,10 @@ __all__ = [
     "MulParams", "NativeUnavailable", "ParameterError", "PeelSplit",
     "StripeSpec", "add", "add_into", "addmul", "bernoulli", "copy_into",
     "copy_out", "create", "default_params", "equal", "first_difference",
-    "from_dense", "from_host", "from_numpy", "identity", "launch_count",
+    "from_dense", "from_host", "from_numpy", "get_engine", "identity",
+    "launch_count",
     "mul_m4rm", "mul_m4rm_blocked", "mul_m4rm_into", "mul_m4rm_multitable",
-    "mul_strassen", "peel_split", "random", "tail_mask", "to_dense",
+    "mul_strassen", "peel_split", "random", "set_engine", "tail_mask",
+    "to_dense",
     "to_numpy", "trailing_bits_clean", "window", "words_per_row", "zero_into",
 ]

@@ -61,6 +61,8 @@ SIGNATURES = {
                        + [ctypes.POINTER(ctypes.c_int64)]),
     "gf2_launch_count": (ctypes.c_int64, []),
     "gf2_timer_enable": (ctypes.c_int, [ctypes.c_int]),
+    "gf2_set_engine": (ctypes.c_int, [ctypes.c_int]),
+    "gf2_get_engine": (ctypes.c_int, []),
     "gf2_timer_read": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_int64)]),
@@ -140,3 +142,19 @@ def timer_read():
     check(load().gf2_timer_read(ctypes.byref(ms), ctypes.byref(ops),
                                 ctypes.byref(n)))
     return ms.value, ops.value, n.value
+
+
+ENGINES = {"m4rm": 0, "tc-i8": 1, "tc-f8": 2}
+
+
+def set_engine(name: str) -> None:
+    """Select the product engine: "m4rm" (shared-memory Gray tables),
+    "tc-i8" or "tc-f8" (tcgen05 tensor cores). Results are identical."""
+    if name not in ENGINES:
+        raise ValueError(f"engine {name!r} not in {sorted(ENGINES)}")
+    check(load().gf2_set_engine(ENGINES[name]))
+
+
+def get_engine() -> str:
+    e = int(load().gf2_get_engine())
+    return {v: k for k, v in ENGINES.items()}[e]

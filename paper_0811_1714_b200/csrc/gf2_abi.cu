@@ -14,6 +14,7 @@ int strassen_mul(const gf2_view &C, const gf2_view &A, const gf2_view &B, int64_
 void peel_split(int64_t m, int64_t l, int64_t n, int64_t cutoff, int64_t out[4]);
 
 std::atomic<int64_t> g_launches{0};
+int g_engine = 0;
 static thread_local std::string t_err;
 
 int set_error(int code, const std::string &msg) {
@@ -95,6 +96,14 @@ int64_t gf2_pitch_words(int64_t ncols) {
 int64_t gf2_launch_count(void) { return g_launches.load(); }
 
 int gf2_timer_enable(int on) { return timer_enable(on); }
+
+int gf2_set_engine(int engine) {
+    if (engine < 0 || engine > 2) return set_error(GF2_ERR_PARAMETER, "engine must be 0 (m4rm), 1 (tc-i8), 2 (tc-f8)");
+    g_engine = engine;
+    return GF2_OK;
+}
+
+int gf2_get_engine(void) { return g_engine; }
 
 int gf2_timer_read(double *kernel_ms, double *bitops, int64_t *launches) {
     return timer_read(kernel_ms, bitops, launches);

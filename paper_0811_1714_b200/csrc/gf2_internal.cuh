@@ -82,6 +82,13 @@ struct M4rmBatch {
     int accumulate;
 };
 int launch_m4rm(const M4rmBatch &b, cudaStream_t s);
+int launch_umma(const M4rmBatch &b, int kind, cudaStream_t s);
+// multiply engine for every product (gf2_set_engine): 0 M4RM, 1 tcgen05 i8, 2 tcgen05 f8
+extern int g_engine;
+inline int launch_product(const M4rmBatch &b, cudaStream_t s) {
+    if (g_engine == 0) return launch_m4rm(b, s);
+    return launch_umma(b, g_engine == 1 ? 0 : 1, s);
+}
 int timer_enable(int on);
 int timer_read(double *ms, double *bitops, int64_t *launches);
 

@@ -54,7 +54,7 @@ int pool_setup() {
 int m4rm_view(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accumulate, cudaStream_t s) {
     M4rmBatch mb{a.data, a.pitch, 0, b.data, b.pitch, 0, c.data, c.pitch, 0,
                  a.nrows,  a.ncols, b.ncols, 1, accumulate};
-    return launch_m4rm(mb, s);
+    return launch_product(mb, s);
 }
 
 int strassen_core(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0, int depth, int accumulate,
@@ -127,7 +127,7 @@ int strassen_core(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0, in
                      ws + offB[depth], Nw[depth], L[depth] * Nw[depth],
                      ws + offC[depth], Nw[depth], M[depth] * Nw[depth],
                      M[depth], L[depth], N[depth], P[depth], 0};
-        rc = launch_m4rm(mb, s);
+        rc = launch_product(mb, s);
     }
     // ---- post-combination, deepest level first
     for (int lv = depth - 1; lv >= 0 && rc == GF2_OK; --lv) {

@@ -1,0 +1,439 @@
+// Tensor-core GF(2) contraction on sm_100a (north_star (c)).
+//
+// C (^)= A.B over GF(2) as an integer product with the sum reduced mod 2:
+//   1. k_expand: packed bits -> one byte per entry (0 or ONE), A row-major
+//      (K contiguous) and B row-major (N contiguous) -- no transpose needed,
+//      B is consumed MN-major by the MMA.
+//   2. k_umma: persistent TMA -> tcgen05.mma -> TMEM pipeline.
+//        warp 0  : TMA producer (3 boxes per stage: A 128x128, B 2 x 128x128)
+//        warp 1  : MMA issuer, tcgen05.mma.cta_group::1 M=128 N=256 K=32
+//        warp 2  : TMEM allocator (512 columns = two 256-column accumulators)
+//        warps 4-7: epilogue: tcgen05.ld 32x32b.x32 -> parity -> 32-bit packs
+//                   (column c0+j -> bit 31-j, the reference's MSB-first order)
+//                   -> store / XOR / red.xor into C.
+//      Smem operands use the 128-byte swizzle: A K-major (8-row atoms,
+//      SBO 1024), B MN-major (8-k-row atoms of 128 N bytes, SBO 1024, the two
+//      128-column halves LBO = 16 KiB apart).
+//   kind::i8 (u8 0/1, s32 accumulators) is exact by construction (even mod
+//   2^32 the LSB is right). kind::f8f6f4 (e4m3 1.0 = 0x38, f32 accumulators)
+//   is exact while partial sums stay integers representable in the
+//   accumulator: K is cut into chunks of <= 8192 whose parities are XORed
+//   (red.global.xor), far inside the 2^24 f32 integer range.
+#include <cuda.h>
+
+#include <vector>
+
+#include "gf2_internal.cuh"
+
+namespace gf2 {
+
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 128;
+constexpr int STAGES = 4;
+constexpr int A_STAGE = BM * BK;          // 16 KiB
+constexpr int B_STAGE = BN * BK;          // 32 KiB
+constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
+constexpr int UMMA_THREADS = 256;
+constexpr int64_t F8_KCHUNK = 8192;
+
+// ------------------------------------------------------------------ PTX
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                            uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(dst),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+// UMMA shared-memory descriptor (sm_100 "version 1"), 128-byte swizzle.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= 1ull << 46;  // version
+    d |= 2ull << 61;  // SWIZZLE_128B
+    return d;
+}
+
+template <int KIND>  // 0: kind::i8 (u8 x u8 -> s32), 1: kind::f8f6f4 (e4m3 -> f32)
+__device__ __forceinline__ void umma(uint32_t taddr, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    if (KIND == 0)
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(taddr),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+    else
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(taddr),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+                 : "memory");
+}
+
+#define TMEM_LD32(taddr, r)                                                                                    \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"  \
+                 "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"              \
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),        \
+                   "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),    \
+                   "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), \
+                   "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), \
+                   "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                          \
+                 : "r"(taddr))
+
+// ------------------------------------------------------------------ expand
+// bits -> bytes (0 or `one`), 64 entries per thread; batched over problems.
+__global__ void k_expand(const u64 *__restrict__ src, int64_t sp, int64_t sstride, uint8_t *__restrict__ dst,
+                         int64_t dp, int64_t dstride, int64_t rows, int64_t cols, uint32_t one) {
+    const int64_t width = words_per_row(cols);
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= width) return;
+    const u64 tm = (j == width - 1) ? tail_mask(cols) : ~0ULL;
+    const u64 *s = src + (int64_t)blockIdx.z * sstride;
+    uint8_t *d = dst + (int64_t)blockIdx.z * dstride;
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+        const u64 x = s[r * sp + j] & tm;
+        uint8_t *drow = d + r * dp + j * 64;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (j * 64 + c * 16 >= dp) break;
+            const uint32_t h16 = (uint32_t)(x >> (48 - 16 * c)) & 0xFFFFu;
+            const uint32_t rv = __brev(h16) >> 16;  // entry 16c+i at bit i
+            uint4 v;
+            v.x = (((rv >> 0) & 0xF) * 0x00204081u & 0x01010101u) * one;
+            v.y = (((rv >> 4) & 0xF) * 0x00204081u & 0x01010101u) * one;
+            v.z = (((rv >> 8) & 0xF) * 0x00204081u & 0x01010101u) * one;
+            v.w = (((rv >> 12) & 0xF) * 0x00204081u & 0x01010101u) * one;
+            *reinterpret_cast<uint4 *>(drow + c * 16) = v;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ gemm
+struct UArgs {
+    u64 *C;
+    int64_t pc, sc;
+    int64_t m, n, Wn;
+    int mt, nt, kblocks, kchunk_blocks, nchunks;
+    int64_t nprob;
+    int mode;  // 0 store, 1 xor, 2 atomic xor
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(UMMA_THREADS, 1)
+    k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, UArgs p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-byte alignment for the 128-byte swizzle atoms
+    const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    const uint32_t sA = base_u32;
+    const uint32_t sB = base_u32 + STAGES * A_STAGE;
+    const uint32_t sBar = sB + STAGES * B_STAGE;
+    const uint32_t bar_full = sBar, bar_empty = sBar + 8 * STAGES, bar_tfull = sBar + 16 * STAGES,
+                   bar_tempty = bar_tfull + 16;
+    const uint32_t tmem_holder = bar_tempty + 16;
+    unsigned char *gen_base = smem_raw + (base_u32 - smem_u32(smem_raw));
+    volatile uint32_t *tmem_holder_ptr = reinterpret_cast<volatile uint32_t *>(gen_base + (tmem_holder - base_u32));
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(bar_full + 8 * s, 1);
+            mbar_init(bar_empty + 8 * s, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(bar_tfull + 8 * b, 1);
+            mbar_init(bar_tempty + 8 * b, 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(tmem_holder)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder_ptr;
+
+    const int64_t tiles_per_chunk = p.nprob * p.mt * p.nt;
+    const int64_t ntiles = tiles_per_chunk * p.nchunks;
+
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int chunk = (int)(t / tiles_per_chunk);
+            int64_t r = t % tiles_per_chunk;
+            const int prob = (int)(r / (p.mt * p.nt));
+            r %= (p.mt * p.nt);
+            const int mtile = (int)(r / p.nt), ntile = (int)(r % p.nt);
+            const int kb0 = chunk * p.kchunk_blocks;
+            const int kb1 = min(kb0 + p.kchunk_blocks, p.kblocks);
+            for (int kb = kb0; kb < kb1; ++kb) {
+                mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+                mbar_expect_tx(bar_full + 8 * stage, STAGE_BYTES);
+                tma_load_3d(sA + stage * A_STAGE, &tmA, kb * BK, mtile * BM, prob, bar_full + 8 * stage);
+                tma_load_3d(sB + stage * B_STAGE, &tmB, ntile * BN, kb * BK, prob, bar_full + 8 * stage);
+                tma_load_3d(sB + stage * B_STAGE + B_STAGE / 2, &tmB, ntile * BN + 128, kb * BK, prob,
+                            bar_full + 8 * stage);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---------------- MMA issuer
+        // instruction descriptor: D format, A/B formats, B MN-major, N, M
+        const uint32_t idesc = (KIND == 0 ? (2u << 4) : (1u << 4)) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) |
+                               ((uint32_t)(BM >> 4) << 24);
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            const int chunk = (int)(t / tiles_per_chunk);
+            const int kb0 = chunk * p.kchunk_blocks;
+            const int kb1 = min(kb0 + p.kchunk_blocks, p.kblocks);
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            mbar_wait(bar_tempty + 8 * acc, acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + acc * BN;
+            for (int kb = kb0; kb < kb1; ++kb) {
+                mbar_wait(bar_full + 8 * stage, phase);
+                tc_fence_after();
+#pragma unroll
+                for (int k = 0; k < BK / 32; ++k) {
+                    const uint64_t ad = smem_desc(sA + stage * A_STAGE + k * 32, 16, 1024);
+                    const uint64_t bd = smem_desc(sB + stage * B_STAGE + k * 32 * 128, B_STAGE / 2, 1024);
+                    umma<KIND>(taddr, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                }
+                umma_commit(bar_empty + 8 * stage);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            umma_commit(bar_tfull + 8 * acc);
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue: TMEM -> parity bits -> C
+        const int q = warp & 3;  // TMEM lane quadrant
+        int it = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            int64_t r = t % tiles_per_chunk;
+            const int prob = (int)(r / (p.mt * p.nt));
+            r %= (p.mt * p.nt);
+            const int mtile = (int)(r / p.nt), ntile = (int)(r % p.nt);
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            mbar_wait(bar_tfull + 8 * acc, acc_phase);
+            tc_fence_after();
+            uint32_t packed[BN / 32];
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t v[32];
+                TMEM_LD32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                uint32_t pk = 0;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    uint32_t bit;
+                    if (KIND == 0)
+                        bit = v[j] & 1u;
+                    else
+                        bit = __float_as_uint(__uint_as_float(v[j]) + 8388608.0f) & 1u;
+                    pk = (pk << 1) | bit;
+                }
+                packed[c] = pk;
+            }
+            tc_fence_before();
+            mbar_arrive(bar_tempty + 8 * acc);
+            const int64_t row = (int64_t)mtile * BM + q * 32 + lane;
+            if (row < p.m) {
+                u64 *crow = p.C + prob * p.sc + row * p.pc;
+                const u64 ctm = tail_mask(p.n);
+#pragma unroll
+                for (int w = 0; w < BN / 64; ++w) {
+                    const int64_t wi = (int64_t)ntile * (BN / 64) + w;
+                    if (wi >= p.Wn) break;
+                    const u64 v = ((u64)packed[2 * w] << 32) | (u64)packed[2 * w + 1];
+                    if (p.mode == 2) {
+                        if (v) atomicXor(reinterpret_cast<unsigned long long *>(crow + wi), (unsigned long long)v);
+                    } else if (p.mode == 1) {
+                        crow[wi] ^= v;
+                    } else if (wi == p.Wn - 1 && ctm != ~0ULL) {
+                        crow[wi] = (crow[wi] & ~ctm) | v;
+                    } else {
+                        crow[wi] = v;
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem_base) : "memory");
+    }
+}
+
+// ------------------------------------------------------------------ host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+
+int get_encode() {
+    if (g_encode) return GF2_OK;
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !fn || q != cudaDriverEntryPointSuccess)
+        return set_error(GF2_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    g_encode = (EncodeTiledFn)fn;
+    return GF2_OK;
+}
+
+// 3-D byte tensor (inner, outer, problems) with a 128 x 128 box, 128-byte swizzle.
+int make_map(CUtensorMap *map, void *base, uint64_t inner, uint64_t outer, uint64_t nprob, uint64_t pitch,
+             uint64_t pstride) {
+    GF2_TRY(get_encode());
+    cuuint64_t dims[3] = {inner, outer, nprob};
+    cuuint64_t strides[2] = {pitch, pstride};
+    cuuint32_t box[3] = {128, 128, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(GF2_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return GF2_OK;
+}
+
+int g_sms = 0;
+
+}  // namespace
+
+int launch_expand(const u64 *src, int64_t sp, int64_t sstride, uint8_t *dst, int64_t dp, int64_t dstride,
+                  int64_t rows, int64_t cols, int64_t nprob, uint32_t one, cudaStream_t s) {
+    const int64_t width = words_per_row(cols);
+    if (!rows || !width || !nprob) return GF2_OK;
+    dim3 blk((unsigned)(width >= 128 ? 128 : (width >= 32 ? 32 : width)));
+    dim3 grd((unsigned)((width + blk.x - 1) / blk.x), (unsigned)(rows > 65535 ? 65535 : rows), (unsigned)nprob);
+    k_expand<<<grd, blk, 0, s>>>(src, sp, sstride, dst, dp, dstride, rows, cols, one);
+    note_launch();
+    return check_cuda(cudaGetLastError(), "k_expand launch");
+}
+
+// C (^)= A.B for a batch of problems via byte expansion + tcgen05. kind: 0 i8, 1 f8.
+int launch_umma(const M4rmBatch &b, int kind, cudaStream_t s) {
+    if (!b.m || !b.n || !b.nprob) return GF2_OK;
+    if (b.l == 0) {
+        if (b.accumulate) return GF2_OK;
+        for (int64_t q = 0; q < b.nprob; ++q) {
+            gf2_view v{b.C + q * b.sc, b.pc, b.m, b.n};
+            GF2_TRY(launch_ewise(v, nullptr, nullptr, 0, s));
+        }
+        return GF2_OK;
+    }
+    if (b.nprob > 65535) return set_error(GF2_ERR_PARAMETER, "too many problems for the tensor-core path");
+    if (!g_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES),
+                           "umma smem attr"));
+        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES),
+                           "umma smem attr"));
+    }
+    const int64_t kp = (b.l + 15) / 16 * 16, np = (b.n + 15) / 16 * 16;
+    const int64_t a_bytes = b.nprob * b.m * kp, b_bytes = b.nprob * b.l * np;
+    uint8_t *ws = nullptr;
+    cudaError_t e = cudaMallocAsync((void **)&ws, (size_t)(a_bytes + b_bytes), s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(GF2_ERR_OOM, std::string("umma workspace: ") + cudaGetErrorString(e));
+    }
+    uint8_t *a8 = ws, *b8 = ws + a_bytes;
+    const uint32_t one = kind == 0 ? 0x01u : 0x38u;
+    int rc = launch_expand(b.A, b.pa, b.sa, a8, kp, b.m * kp, b.m, b.l, b.nprob, one, s);
+    if (rc == GF2_OK) rc = launch_expand(b.B, b.pb, b.sb, b8, np, b.l * np, b.l, b.n, b.nprob, one, s);
+    CUtensorMap ta, tb;
+    if (rc == GF2_OK) rc = make_map(&ta, a8, (uint64_t)b.l, (uint64_t)b.m, (uint64_t)b.nprob, kp, b.m * kp);
+    if (rc == GF2_OK) rc = make_map(&tb, b8, (uint64_t)b.n, (uint64_t)b.l, (uint64_t)b.nprob, np, b.l * np);
+    if (rc == GF2_OK) {
+        UArgs ua{};
+        ua.C = b.C;
+        ua.pc = b.pc;
+        ua.sc = b.sc;
+        ua.m = b.m;
+        ua.n = b.n;
+        ua.Wn = words_per_row(b.n);
+        ua.mt = (int)((b.m + BM - 1) / BM);
+        ua.nt = (int)((b.n + BN - 1) / BN);
+        ua.kblocks = (int)((b.l + BK - 1) / BK);
+        ua.kchunk_blocks = kind == 0 ? ua.kblocks : (int)(F8_KCHUNK / BK);
+        ua.nchunks = (ua.kblocks + ua.kchunk_blocks - 1) / ua.kchunk_blocks;
+        ua.nprob = b.nprob;
+        if (ua.nchunks > 1) {
+            if (!b.accumulate) {
+                for (int64_t q = 0; q < b.nprob && rc == GF2_OK; ++q) {
+                    gf2_view v{b.C + q * b.sc, b.pc, b.m, b.n};
+                    rc = launch_ewise(v, nullptr, nullptr, 0, s);
+                }
+            }
+            ua.mode = 2;
+        } else {
+            ua.mode = b.accumulate ? 1 : 0;
+        }
+        const int64_t ntiles = (int64_t)ua.nchunks * b.nprob * ua.mt * ua.nt;
+        const int grid = (int)(ntiles < g_sms ? ntiles : g_sms);
+        if (rc == GF2_OK) {
+            if (kind == 0)
+                k_umma<0><<<grid, UMMA_THREADS, SMEM_BYTES, s>>>(ta, tb, ua);
+            else
+                k_umma<1><<<grid, UMMA_THREADS, SMEM_BYTES, s>>>(ta, tb, ua);
+            note_launch();
+            rc = check_cuda(cudaGetLastError(), "k_umma launch");
+        }
+    }
+    cudaFreeAsync(ws, s);
+    return rc;
+}
+
+}  // namespace gf2

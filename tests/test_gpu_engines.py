@@ -1,0 +1,103 @@
+"""Parity of the tcgen05 tensor-core engines (kind::i8, kind::f8f6f4) with
+the oracle: the same product as M4RM, bit-exact including trailing bits."""
+
+import numpy as np
+import pytest
+
+from oracle import gf2_oracle as O
+from oracle import gf2_port as P
+
+pytestmark = pytest.mark.gpu
+g = pytest.importorskip("paper_0811_1714_b200")
+
+ENGINES = ["tc-i8", "tc-f8"]
+
+
+@pytest.fixture(autouse=True)
+def _engine_reset():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    yield
+    g.set_engine("m4rm")
+
+
+def words(m):
+    return m.to_numpy()
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_small_and_ragged(engine):
+    g.set_engine(engine)
+    rng = np.random.default_rng(5)
+    for trial in range(25):
+        m, l, n = (int(x) for x in rng.integers(1, 700, 3))
+        a, b = g.random(m, l, trial + 1), g.random(l, n, trial + 2)
+        want = O.naive_product(O.random(m, l, trial + 1), O.random(l, n, trial + 2))
+        c = g.mul_m4rm(a, b, 8)
+        assert np.array_equal(words(c), want.words), (engine, m, l, n)
+        assert g.trailing_bits_clean(c)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_golden_and_windows(engine, golden):
+    g.set_engine(engine)
+    for i, m, l, n, sa, sb in golden["prod_cases"].tolist():
+        a, b = g.random(m, l, sa), g.random(l, n, sb)
+        assert np.array_equal(words(g.mul_m4rm(a, b, 8)), golden[f"prod_{i}"])
+        assert np.array_equal(words(g.mul_strassen(a, b, g.MulParams(cutoff=64))),
+                              golden[f"prod_{i}"])
+    pa, pb = g.random(90, 640, 77), g.random(700, 512, 78)
+    aw = g.window(pa, 5, 64, 70, 385)
+    bw = g.window(pb, 11, 192, 385, 250)
+    assert np.array_equal(words(g.mul_m4rm(aw, bw, 8)), golden["win_product"])
+    pc = g.random(80, 512, 79)
+    g.addmul(g.window(pc, 3, 64, 70, 250), aw, bw, g.MulParams(cutoff=64))
+    assert np.array_equal(words(pc), golden["win_accum_parent"])
+    a, b, c = g.random(150, 333, 91), g.random(333, 200, 92), g.random(150, 200, 93)
+    g.mul_m4rm_into(c, a, b, 8, 64, 4)
+    assert np.array_equal(words(c), golden["into_result"])
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_adversarial_large_sums(engine):
+    """Rows of ones against columns of odd popcount near K: the f8 path's
+    fp32 partial sums are as large as possible (K chunked at 8192)."""
+    g.set_engine(engine)
+    for l in (4096, 8192, 20000):
+        ones = np.full((128, O.words_per_row(l)), np.uint64(0xFFFFFFFFFFFFFFFF))
+        ones[:, -1] &= np.uint64(O.tail_mask(l))
+        a = g.from_numpy(ones, l)
+        dense_b = np.ones((l, 300), dtype=np.uint8)
+        dense_b[0, ::2] = 0
+        dense_b[5, ::3] = 0
+        b = g.from_dense(dense_b)
+        want = dense_b.sum(0) & 1
+        got = g.to_dense(g.mul_m4rm(a, b, 8))
+        assert np.array_equal(got, np.tile(want, (128, 1))), (engine, l)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_configs(engine, digests):
+    g.set_engine(engine)
+    a, b = g.random(1024, 1024, 11), g.random(1024, 1024, 12)
+    assert O.digest(words(g.mul_m4rm(a, b, 8))) == digests["cfg1"]
+    a, b = g.random(4096, 4096, 21), g.random(4096, 4096, 22)
+    assert O.digest(words(g.mul_strassen(a, b, g.MulParams(cutoff=1024, k=8)))) == digests["cfg2"]
+    a, b = g.random(16384, 16384, 31), g.random(16384, 16384, 32)
+    assert O.digest(words(g.mul_strassen(a, b))) == digests["cfg3"]
+    assert O.digest(words(g.mul_m4rm(a, b, 8))) == digests["cfg3"]
+    t = O.bernoulli_threshold(0.1)
+    a = g.bernoulli(10000, 7001, 41, threshold=t)
+    b = g.bernoulli(7001, 12345, 42, threshold=t)
+    assert O.digest(words(g.mul_strassen(a, b))) == digests["cfg4_product"]
+    c0 = g.random(10000, 12345, 43)
+    g.addmul(c0, a, b)
+    assert O.digest(words(c0)) == digests["cfg4_addmul"]
+
+
+def test_engine_switch_validation():
+    with pytest.raises(ValueError):
+        g.set_engine("nope")
+    g.set_engine("tc-f8")
+    assert g.get_engine() == "tc-f8"
