@@ -44,7 +44,7 @@ def parse():
     p.add_argument("--cutoff", type=int, default=0,
                    help="Strassen cutoff (0 = device default)")
     p.add_argument("--npanels", type=int, default=4)
-    p.add_argument("--engine", default="m4rm", choices=["m4rm", "tc-i8", "tc-f8"],
+    p.add_argument("--engine", default="tc-i8", choices=["m4rm", "tc-i8", "tc-f8"],
                    help="product engine (results are identical)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -350,24 +350,40 @@ def main():
     nsm = props.multi_processor_count
     smem_peak_gbs = 128.0 * nsm * sm_max * 1e6 / 1e9   # 128 B/clk/SM crossbar
     roofline = None
-    if kern_n:
+    if kern_n and args.engine == "m4rm":
         lut_bytes = kern_ops / 64.0      # W/(8k) bytes, k = 8
         ach = lut_bytes / (kern_ms * 1e-3) / 1e9
         roofline = {
             "bound": "smem", "kernel": "k_m4rm (batched Strassen leaves)",
             "achieved": ach, "peak": smem_peak_gbs, "unit": "GB/s",
             "frac": ach / smem_peak_gbs, "traffic": None,
-            "kernel_ms_per_step": kern_ms / args.steps,
-            "kernel_share_of_step": kern_ms / total_ms if world == 1 else None,
-            "kernel_bitops_per_step": kern_ops / args.steps,
             "peak_source": f"128 B/clk/SM x {nsm} SMs x {sm_max:.0f} MHz "
                            f"(sm_max_mhz from {src}); HBM bound "
                            f"{peaks.get('hbm_gbs')} GB/s never binds here",
         }
+    elif kern_n:
+        # 0/1 bytes through tcgen05 kind::i8 / kind::f8f6f4: 2 ops per MAC
+        ach = 2.0 * kern_ops / (kern_ms * 1e-3) / 1e12
+        peak = 4500.0   # dense 8-bit nominal, B200_PROFILING.md (no measured 8-bit peak)
+        roofline = {
+            "bound": "tensor", "kernel": "k_umma (batched Strassen leaves)",
+            "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+            "frac": ach / peak, "traffic": None,
+            "peak_source": "nominal dense fp8/int8 4.5 PFLOP/s (B200_PROFILING.md); "
+                           "MEASURED_PEAKS bf16 x2 = "
+                           f"{2 * float(peaks.get('bf16_tflops', 0)):.0f} TFLOP/s",
+        }
+    if roofline is not None:
+        roofline.update({
+            "kernel_ms_per_step": kern_ms / args.steps,
+            "kernel_share_of_step": kern_ms / total_ms if world == 1 else None,
+            "kernel_bitops_per_step": kern_ops / args.steps,
+        })
         tr = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tr):
             try:
-                roofline["traffic"] = json.load(open(tr)).get("k_m4rm")
+                key = "k_m4rm" if args.engine == "m4rm" else "k_umma"
+                roofline["traffic"] = json.load(open(tr)).get(key)
             except Exception:
                 pass
     hbm_bytes = 3.0 * m * g.words_per_row(n) * 8
@@ -387,12 +403,13 @@ def main():
                                 f"{w['seed_b']}",
         "config": {"workload": f"{w['name']}: A,B {m}x{l} . {l}x{n} GF(2), "
                                f"Strassen-Winograd (cutoff {params.cutoff}) "
-                               "over M4RM",
+                               f"over the {args.engine} base case",
                    "m": m, "l": l, "n": n, "cutoff": params.cutoff,
                    "parallelism": "single" if world == 1 else
                    f"rows{world} + NCCL broadcast of B ({args.npanels} panels)",
                    "l2": "flushed between timed steps (512 MiB write)"},
         "verified_sha256": verified,
+        "engine": args.engine,
         "gpu_launches": n_launch,
         "gpu_launches_per_step": n_launch / args.steps,
         "clocks": clk,

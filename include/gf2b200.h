@@ -97,6 +97,12 @@ int gf2_copy(const gf2_view *out, const gf2_view *a, void *stream);
 int gf2_m4rm(const gf2_view *c, const gf2_view *a, const gf2_view *b, int k,
              int accumulate, void *stream);
 
+/* One product launch (no recursion) with the current engine (gf2_set_engine):
+ * the dense-contraction entry of north_star (c) when a tensor engine is set.
+ * Same semantics and errors as gf2_m4rm. */
+int gf2_mul(const gf2_view *c, const gf2_view *a, const gf2_view *b,
+            int accumulate, void *stream);
+
 /* strassen.py:257-282 `mul_strassen` (+ peel_split strassen.py:66-84,
  * schedule strassen.py:141-204, peel_fixup strassen.py:219-249):
  * Strassen-Winograd recursion above `cutoff` over an M4RM base case.
@@ -118,9 +124,10 @@ int64_t gf2_launch_count(void);
  * and returns the summed kernel milliseconds, the algorithmic bit-ops
  * (m*l*n per product) those launches computed, and the launch count. */
 int gf2_timer_enable(int on);
-/* Engine for every product (M4RM calls and Strassen leaves), process-wide:
- * 0 = M4RM shared-memory Gray tables (default), 1 = tcgen05 kind::i8,
- * 2 = tcgen05 kind::f8f6f4 (e4m3 0/1). Results are identical. */
+/* Engine for Strassen leaves, non-recursive gf2_strassen calls and gf2_mul,
+ * process-wide: 0 = M4RM shared-memory Gray tables, 1 = tcgen05 kind::i8
+ * (default: measured fastest), 2 = tcgen05 kind::f8f6f4 (e4m3 0/1).
+ * gf2_m4rm always runs the M4RM kernel. Results are identical. */
 int gf2_set_engine(int engine);
 int gf2_get_engine(void);
 int gf2_timer_read(double *kernel_ms, double *bitops, int64_t *launches);

@@ -20,7 +20,8 @@ from .errors import (AlignmentError, DimensionError, FormatError, GF2MatError,
 from .m4rm import (StripeSpec, mul_m4rm, mul_m4rm_blocked, mul_m4rm_into,
                    mul_m4rm_multitable)
 from .strassen import (GPU_CUTOFF, MulParams, PeelSplit, addmul,
-                       default_params, mul_strassen, peel_split)
+                       addmul_direct, default_params, mul_direct,
+                       mul_strassen, peel_split)
 
 __version__ = "0.1.0"
 
@@ -28,11 +29,11 @@ __all__ = [
     "AlignmentError", "BitMatrix", "DeviceError", "DimensionError",
     "FormatError", "GF2MatError", "GPU_CUTOFF", "HostMatrix", "MatrixWindow",
     "MulParams", "NativeUnavailable", "ParameterError", "PeelSplit",
-    "StripeSpec", "add", "add_into", "addmul", "bernoulli", "copy_into",
+    "StripeSpec", "add", "add_into", "addmul", "addmul_direct", "bernoulli", "copy_into",
     "copy_out", "create", "default_params", "equal", "first_difference",
     "from_dense", "from_host", "from_numpy", "get_engine", "identity",
     "launch_count",
-    "mul_m4rm", "mul_m4rm_blocked", "mul_m4rm_into", "mul_m4rm_multitable",
+    "mul_direct", "mul_m4rm", "mul_m4rm_blocked", "mul_m4rm_into", "mul_m4rm_multitable",
     "mul_strassen", "peel_split", "random", "set_engine", "tail_mask",
     "to_dense",
     "to_numpy", "trailing_bits_clean", "window", "words_per_row", "zero_into",

@@ -55,6 +55,7 @@ SIGNATURES = {
     "gf2_add": (ctypes.c_int, [_V, _V, _V, _P]),
     "gf2_copy": (ctypes.c_int, [_V, _V, _P]),
     "gf2_m4rm": (ctypes.c_int, [_V, _V, _V, ctypes.c_int, ctypes.c_int, _P]),
+    "gf2_mul": (ctypes.c_int, [_V, _V, _V, ctypes.c_int, _P]),
     "gf2_strassen": (ctypes.c_int, [_V, _V, _V, ctypes.c_int64, ctypes.c_int,
                                     ctypes.c_int, _P]),
     "gf2_peel_split": (ctypes.c_int, [ctypes.c_int64] * 4

@@ -51,7 +51,8 @@ class BitMatrix:
 
     __slots__ = ("nrows", "ncols", "width", "pitch", "storage", "__weakref__")
 
-    def __init__(self, nrows: int, ncols: int, device=None):
+    def __init__(self, nrows: int, ncols: int, device=None,
+                 _overwritten: bool = False):
         if nrows < 0 or ncols < 0:
             raise DimensionError(f"negative dimensions {nrows}x{ncols}")
         lib = _lib.lib_cuda()
@@ -62,8 +63,14 @@ class BitMatrix:
         self.pitch = int(lib.gf2_pitch_words(ncols))
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device())
-        self.storage = torch.zeros((self.nrows, self.pitch), dtype=torch.int64,
-                                   device=device)
+        if _overwritten and self.pitch == self.width and ncols % 64 == 0:
+            # a product target whose every word the kernels overwrite whole
+            # (no padding words, no partial last word to merge into): no fill
+            self.storage = torch.empty((self.nrows, self.pitch),
+                                       dtype=torch.int64, device=device)
+        else:
+            self.storage = torch.zeros((self.nrows, self.pitch),
+                                       dtype=torch.int64, device=device)
 
     # reference-compatible accessors
     @property

@@ -9,12 +9,13 @@
 
 namespace gf2 {
 int m4rm_mul(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accumulate, cudaStream_t s);
+int engine_mul(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accumulate, cudaStream_t s);
 int strassen_mul(const gf2_view &C, const gf2_view &A, const gf2_view &B, int64_t cutoff, int accumulate,
                  cudaStream_t s);
 void peel_split(int64_t m, int64_t l, int64_t n, int64_t cutoff, int64_t out[4]);
 
 std::atomic<int64_t> g_launches{0};
-int g_engine = 0;
+int g_engine = 1;  // tcgen05 kind::i8: measured fastest base case
 static thread_local std::string t_err;
 
 int set_error(int code, const std::string &msg) {
@@ -195,6 +196,11 @@ int gf2_m4rm(const gf2_view *c, const gf2_view *a, const gf2_view *b, int k, int
     if (k < 1 || k > 16) return set_error(GF2_ERR_PARAMETER, "k=" + std::to_string(k) + " outside 1..16");
     GF2_TRY(check_mul(c, a, b));
     return m4rm_mul(*c, *a, *b, accumulate ? 1 : 0, (cudaStream_t)stream);
+}
+
+int gf2_mul(const gf2_view *c, const gf2_view *a, const gf2_view *b, int accumulate, void *stream) {
+    GF2_TRY(check_mul(c, a, b));
+    return engine_mul(*c, *a, *b, accumulate ? 1 : 0, (cudaStream_t)stream);
 }
 
 int gf2_strassen(const gf2_view *c, const gf2_view *a, const gf2_view *b, int64_t cutoff, int k, int accumulate,

@@ -83,6 +83,22 @@ struct M4rmBatch {
 };
 int launch_m4rm(const M4rmBatch &b, cudaStream_t s);
 int launch_umma(const M4rmBatch &b, int kind, cudaStream_t s);
+// Tensor-core batch with the last Strassen level fused: fuse_pre -> product
+// q = 7p + i multiplies XORs of source problem p's quadrants (maskA/maskB);
+// fuse_post -> its result is XORed into quadrants maskC[i] of C problem p.
+struct UmmaJob {
+    const u64 *A;
+    int64_t pa, sa;
+    const u64 *B;
+    int64_t pb, sb;
+    u64 *C;
+    int64_t pc, sc;
+    int64_t m, l, n;  // product (leaf) dimensions
+    int64_t nsrc;     // source problems (x7 products when fuse_pre)
+    int fuse_pre, fuse_post, accumulate;
+    unsigned maskA[7], maskB[7], maskC[7];
+};
+int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s);
 // multiply engine for every product (gf2_set_engine): 0 M4RM, 1 tcgen05 i8, 2 tcgen05 f8
 extern int g_engine;
 inline int launch_product(const M4rmBatch &b, cudaStream_t s) {
@@ -90,6 +106,8 @@ inline int launch_product(const M4rmBatch &b, cudaStream_t s) {
     return launch_umma(b, g_engine == 1 ? 0 : 1, s);
 }
 int timer_enable(int on);
+int timer_begin(cudaStream_t s, double bitops);  // -1 when the timer is off
+void timer_end(int idx, cudaStream_t s);
 int timer_read(double *ms, double *bitops, int64_t *launches);
 
 }  // namespace gf2

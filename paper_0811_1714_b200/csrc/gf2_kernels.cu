@@ -2,6 +2,8 @@
 // XOR-combine behind the breadth-first Strassen-Winograd schedule.
 // All are HBM-bound streaming kernels: one 64-bit word per thread, warps
 // running along a row so every access is a coalesced 256-byte segment.
+#include <type_traits>
+
 #include "gf2_internal.cuh"
 
 namespace gf2 {
@@ -74,26 +76,69 @@ __global__ void k_ewise(u64 *out, int64_t po, const u64 *a, int64_t pa, const u6
     }
 }
 
+// VEC words per thread (2 = 16-byte accesses when everything is 16-byte
+// aligned), ROWS rows per thread with all loads issued before the stores.
+template <int VEC, int ROWS>
 __global__ void k_combine(CombineArgs p, int64_t wblocks) {
-    int64_t o = blockIdx.x / wblocks;
-    int64_t j = (blockIdx.x % wblocks) * blockDim.x + threadIdx.x;
+    typedef typename std::conditional<VEC == 2, ulonglong2, unsigned long long>::type V;
+    const int64_t o = blockIdx.x / wblocks;
+    const int64_t j = ((blockIdx.x % wblocks) * blockDim.x + threadIdx.x) * VEC;
     if (j >= p.W) return;
-    int64_t prob = o / p.nq;
-    int q = (int)(o % p.nq);
-    unsigned mask = p.mask[q];
+    const int64_t prob = o / p.nq;
+    const int q = (int)(o % p.nq);
+    const unsigned mask = p.mask[q];
     const u64 *sbase = p.src + prob * p.src_stride;
     u64 *d = p.dst + prob * p.dst_stride + p.dst_off[q];
-    for (int64_t r = (int64_t)blockIdx.y * blockDim.y + threadIdx.y; r < p.R;
-         r += (int64_t)gridDim.y * blockDim.y) {
-        u64 v = 0;
+    for (int64_t r0 = (int64_t)blockIdx.y * blockDim.y * ROWS + threadIdx.y; r0 < p.R;
+         r0 += (int64_t)gridDim.y * blockDim.y * ROWS) {
+        V v[ROWS];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-            if (mask & (1u << i)) v ^= __ldg(sbase + p.src_off[i] + r * p.src_pitch + j);
-        u64 *dp = d + r * p.dst_pitch + j;
-        if (p.accumulate)
-            *dp ^= v;
-        else
-            *dp = v;
+        for (int k = 0; k < ROWS; ++k) {
+            const int64_t r = r0 + (int64_t)k * blockDim.y;
+            if (VEC == 2) {
+                ulonglong2 acc = make_ulonglong2(0, 0);
+                if (r < p.R) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        if (mask & (1u << i)) {
+                            const ulonglong2 x =
+                                __ldg(reinterpret_cast<const ulonglong2 *>(sbase + p.src_off[i] + r * p.src_pitch + j));
+                            acc.x ^= x.x;
+                            acc.y ^= x.y;
+                        }
+                }
+                reinterpret_cast<ulonglong2 *>(v)[k] = acc;
+            } else {
+                unsigned long long acc = 0;
+                if (r < p.R) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        if (mask & (1u << i))
+                            acc ^= __ldg(reinterpret_cast<const unsigned long long *>(sbase + p.src_off[i] +
+                                                                                     r * p.src_pitch + j));
+                }
+                reinterpret_cast<unsigned long long *>(v)[k] = acc;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < ROWS; ++k) {
+            const int64_t r = r0 + (int64_t)k * blockDim.y;
+            if (r >= p.R) break;
+            V *dp = reinterpret_cast<V *>(d + r * p.dst_pitch + j);
+            if (VEC == 2) {
+                ulonglong2 x = reinterpret_cast<ulonglong2 *>(v)[k];
+                if (p.accumulate) {
+                    const ulonglong2 y = *reinterpret_cast<ulonglong2 *>(dp);
+                    x.x ^= y.x;
+                    x.y ^= y.y;
+                }
+                *reinterpret_cast<ulonglong2 *>(dp) = x;
+            } else {
+                unsigned long long x = reinterpret_cast<unsigned long long *>(v)[k];
+                if (p.accumulate) x ^= *reinterpret_cast<unsigned long long *>(dp);
+                *reinterpret_cast<unsigned long long *>(dp) = x;
+            }
+        }
     }
 }
 
@@ -154,12 +199,23 @@ int launch_ewise(const gf2_view &out, const gf2_view *a, const gf2_view *b, int 
 
 int launch_combine(const CombineArgs &a, cudaStream_t s) {
     if (!a.R || !a.W || !a.nprob) return GF2_OK;
-    dim3 blk = row_block(a.W);
-    int64_t wblocks = (a.W + blk.x - 1) / blk.x;
-    int64_t gx = wblocks * a.nprob * a.nq;
-    int64_t gy = (a.R + blk.y - 1) / blk.y;
+    // 16-byte path when every address the kernel forms is 16-byte aligned
+    bool v2 = (a.W % 2 == 0) && ((uintptr_t)a.src % 16 == 0) && ((uintptr_t)a.dst % 16 == 0) &&
+              (a.src_pitch % 2 == 0) && (a.dst_pitch % 2 == 0) && (a.src_stride % 2 == 0) &&
+              (a.dst_stride % 2 == 0);
+    for (int i = 0; i < 8; ++i) v2 = v2 && (a.src_off[i] % 2 == 0) && (a.dst_off[i] % 2 == 0);
+    constexpr int ROWS = 4;
+    const int vec = v2 ? 2 : 1;
+    const int64_t wv = (a.W + vec - 1) / vec;  // vectors per row
+    dim3 blk = row_block(wv);
+    const int64_t wblocks = (wv + blk.x - 1) / blk.x;
+    const int64_t gx = wblocks * a.nprob * a.nq;
+    int64_t gy = (a.R + blk.y * ROWS - 1) / (blk.y * ROWS);
     if (gy > 65535) gy = 65535;
-    k_combine<<<dim3((unsigned)gx, (unsigned)gy, 1), blk, 0, s>>>(a, wblocks);
+    if (v2)
+        k_combine<2, ROWS><<<dim3((unsigned)gx, (unsigned)gy, 1), blk, 0, s>>>(a, wblocks);
+    else
+        k_combine<1, ROWS><<<dim3((unsigned)gx, (unsigned)gy, 1), blk, 0, s>>>(a, wblocks);
     note_launch();
     return check_cuda(cudaGetLastError(), "k_combine launch");
 }

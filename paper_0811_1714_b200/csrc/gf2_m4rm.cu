@@ -329,6 +329,18 @@ int timer_read(double *ms, double *bitops, int64_t *launches) {
     return GF2_OK;
 }
 
+int timer_begin(cudaStream_t s, double bitops) {
+    if (!g_timing) return -1;
+    TimedLaunch tl{pool_event(), pool_event(), bitops};
+    cudaEventRecord(tl.a, s);
+    g_timed.push_back(tl);
+    return (int)g_timed.size() - 1;
+}
+
+void timer_end(int idx, cudaStream_t s) {
+    if (idx >= 0) cudaEventRecord(g_timed[idx].b, s);
+}
+
 int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     if (!b.m || !b.n || !b.nprob) return GF2_OK;
     const int64_t Wn = words_per_row(b.n), Wl = words_per_row(b.l);
@@ -380,13 +392,7 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
         ka.mode = b.accumulate ? 1 : 0;
     }
     const int64_t z = (int64_t)nsplit * b.nprob;
-    TimedLaunch tl{};
-    if (g_timing) {
-        tl.a = pool_event();
-        tl.b = pool_event();
-        tl.bitops = (double)b.m * (double)b.l * (double)b.n * (double)b.nprob;
-        cudaEventRecord(tl.a, s);
-    }
+    const int tidx = timer_begin(s, (double)b.m * (double)b.l * (double)b.n * (double)b.nprob);
     const bool a16 = ((uintptr_t)b.A % 16 == 0) && ((uintptr_t)b.B % 16 == 0) && (b.pa % 2 == 0) &&
                      (b.pb % 2 == 0) && (b.nprob == 1 || (b.sa % 2 == 0 && b.sb % 2 == 0));
     int rc;
@@ -399,10 +405,7 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     else
         rc = a16 ? launch_rpt<4, true>(ka, col_tiles, row_tiles, z, s)
                  : launch_rpt<4, false>(ka, col_tiles, row_tiles, z, s);
-    if (g_timing) {
-        cudaEventRecord(tl.b, s);
-        g_timed.push_back(tl);
-    }
+    timer_end(tidx, s);
     return rc;
 }
 

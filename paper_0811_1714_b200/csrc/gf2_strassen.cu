@@ -57,8 +57,132 @@ int m4rm_view(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accum
     return launch_product(mb, s);
 }
 
+// product q = 7p + i lands in these quadrants of C_p (transpose of kSC)
+constexpr unsigned kSCT[7] = {0xF, 0x1, 0x2, 0x4, 0xA, 0xE, 0xC};
+
+// Tensor-core engine: levels 0..d-2 as below, and the LAST level fused into
+// the product launch -- its pre-additions into the byte expansion, its
+// post-additions into the UMMA epilogue (red.global.xor into C_{d-1}).
+int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0, int depth, int accumulate,
+                     cudaStream_t s) {
+    int64_t M[24], L[24], N[24], Lw[24], Nw[24], P[24];
+    for (int i = 0; i <= depth; ++i) {
+        M[i] = A0.nrows >> i;
+        L[i] = A0.ncols >> i;
+        N[i] = B0.ncols >> i;
+        Lw[i] = L[i] / kWordBits;
+        Nw[i] = N[i] / kWordBits;
+        P[i] = i == 0 ? 1 : P[i - 1] * 7;
+    }
+    const int last = depth - 1;  // deepest materialized level
+    int64_t offA[24], offB[24], offC[24], total = 0;
+    for (int i = 1; i <= last; ++i) {
+        offA[i] = total;
+        total += P[i] * M[i] * Lw[i];
+        offB[i] = total;
+        total += P[i] * L[i] * Nw[i];
+        offC[i] = total;
+        total += P[i] * M[i] * Nw[i];
+    }
+    GF2_TRY(pool_setup());
+    u64 *ws = nullptr;
+    if (total) {
+        cudaError_t e = cudaMallocAsync((void **)&ws, (size_t)total * 8, s);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return set_error(GF2_ERR_OOM, std::string("strassen workspace: ") + cudaGetErrorString(e));
+        }
+    }
+    int rc = GF2_OK;
+    for (int lv = 0; lv < last && rc == GF2_OK; ++lv) {
+        for (int side = 0; side < 2 && rc == GF2_OK; ++side) {
+            CombineArgs c{};
+            const bool isA = side == 0;
+            const int64_t R = isA ? M[lv + 1] : L[lv + 1];
+            const int64_t W = isA ? Lw[lv + 1] : Nw[lv + 1];
+            if (lv == 0) {
+                c.src = isA ? A0.data : B0.data;
+                c.src_pitch = isA ? A0.pitch : B0.pitch;
+            } else {
+                c.src = ws + (isA ? offA[lv] : offB[lv]);
+                c.src_pitch = isA ? Lw[lv] : Nw[lv];
+                c.src_stride = (isA ? M[lv] : L[lv]) * c.src_pitch;
+            }
+            c.src_off[1] = W;
+            c.src_off[2] = R * c.src_pitch;
+            c.src_off[3] = R * c.src_pitch + W;
+            c.dst = ws + (isA ? offA[lv + 1] : offB[lv + 1]);
+            c.dst_pitch = W;
+            c.dst_stride = 7 * R * W;
+            for (int q = 0; q < 7; ++q) {
+                c.dst_off[q] = q * R * W;
+                c.mask[q] = isA ? kSA[q] : kSB[q];
+            }
+            c.nq = 7;
+            c.R = R;
+            c.W = W;
+            c.nprob = P[lv];
+            rc = launch_combine(c, s);
+        }
+    }
+    if (rc == GF2_OK) {
+        UmmaJob jb{};
+        if (last == 0) {
+            jb.A = A0.data; jb.pa = A0.pitch;
+            jb.B = B0.data; jb.pb = B0.pitch;
+            jb.C = C0.data; jb.pc = C0.pitch;
+            if (!accumulate) rc = launch_ewise(C0, nullptr, nullptr, 0, s);
+        } else {
+            jb.A = ws + offA[last]; jb.pa = Lw[last]; jb.sa = M[last] * Lw[last];
+            jb.B = ws + offB[last]; jb.pb = Nw[last]; jb.sb = L[last] * Nw[last];
+            jb.C = ws + offC[last]; jb.pc = Nw[last]; jb.sc = M[last] * Nw[last];
+            rc = check_cuda(cudaMemsetAsync(ws + offC[last], 0, (size_t)(P[last] * M[last] * Nw[last]) * 8, s),
+                            "zero C_{d-1}");
+        }
+        jb.m = M[depth]; jb.l = L[depth]; jb.n = N[depth];
+        jb.nsrc = P[last];
+        jb.fuse_pre = 1;
+        jb.fuse_post = 1;
+        for (int i = 0; i < 7; ++i) {
+            jb.maskA[i] = kSA[i];
+            jb.maskB[i] = kSB[i];
+            jb.maskC[i] = kSCT[i];
+        }
+        if (rc == GF2_OK) rc = launch_umma_job(jb, g_engine == 1 ? 0 : 1, s);
+    }
+    for (int lv = last - 1; lv >= 0 && rc == GF2_OK; --lv) {
+        CombineArgs c{};
+        const int64_t R = M[lv + 1], W = Nw[lv + 1];
+        c.src = ws + offC[lv + 1];
+        c.src_pitch = W;
+        c.src_stride = 7 * R * W;
+        for (int i = 0; i < 7; ++i) c.src_off[i] = i * R * W;
+        if (lv == 0) {
+            c.dst = C0.data;
+            c.dst_pitch = C0.pitch;
+        } else {
+            c.dst = ws + offC[lv];
+            c.dst_pitch = Nw[lv];
+            c.dst_stride = M[lv] * Nw[lv];
+        }
+        c.dst_off[1] = W;
+        c.dst_off[2] = R * c.dst_pitch;
+        c.dst_off[3] = R * c.dst_pitch + W;
+        for (int q = 0; q < 4; ++q) c.mask[q] = kSC[q];
+        c.nq = 4;
+        c.R = R;
+        c.W = W;
+        c.nprob = P[lv];
+        c.accumulate = lv == 0 ? accumulate : 0;
+        rc = launch_combine(c, s);
+    }
+    if (ws) cudaFreeAsync(ws, s);
+    return rc;
+}
+
 int strassen_core(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0, int depth, int accumulate,
                   cudaStream_t s) {
+    if (g_engine != 0) return strassen_core_tc(C0, A0, B0, depth, accumulate, s);
     int64_t M[24], L[24], N[24], Lw[24], Nw[24], P[24];
     for (int i = 0; i <= depth; ++i) {
         M[i] = A0.nrows >> i;
@@ -182,7 +306,14 @@ void peel_split(int64_t m, int64_t l, int64_t n, int64_t cutoff, int64_t out[4])
     out[3] = depth;
 }
 
+// gf2_m4rm: always the M4RM kernel (the named algorithm, m4rm.py:77-121)
 int m4rm_mul(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accumulate, cudaStream_t s) {
+    M4rmBatch mb{a.data, a.pitch, 0, b.data, b.pitch, 0, c.data, c.pitch, 0, a.nrows, a.ncols, b.ncols, 1, accumulate};
+    return launch_m4rm(mb, s);
+}
+
+// gf2_mul: one product launch with the current engine, no recursion
+int engine_mul(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accumulate, cudaStream_t s) {
     return m4rm_view(c, a, b, accumulate, s);
 }
 

@@ -112,29 +112,60 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
                  : "r"(taddr))
 
 // ------------------------------------------------------------------ expand
-// bits -> bytes (0 or `one`), 64 entries per thread; batched over problems.
-__global__ void k_expand(const u64 *__restrict__ src, int64_t sp, int64_t sstride, uint8_t *__restrict__ dst,
-                         int64_t dp, int64_t dstride, int64_t rows, int64_t cols, uint32_t one) {
-    const int64_t width = words_per_row(cols);
+// bits -> bytes (0 or `one`), 64 entries per thread, batched over problems.
+// With fuse = 1 this is also the last Strassen level's pre-addition: output
+// problem q = 7p + i is the XOR of source problem p's quadrants in mask[i].
+struct ExpandArgs {
+    const u64 *src;
+    int64_t sp, sstride;
+    int64_t qoff[4];
+    unsigned mask[7];
+    int fuse;
+    uint8_t *dst;
+    int64_t dp, dstride;
+    int64_t rows, cols;
+    uint32_t one;
+};
+
+// A warp expands 32 consecutive words (2 KiB of bytes): every lane loads one
+// word, then the 128 16-byte chunks are written lane-contiguously (512 B per
+// store instruction) with the source word fetched by shuffle.
+__global__ void k_expand(ExpandArgs a) {
+    const int64_t width = words_per_row(a.cols);
+    const int lane = threadIdx.x & 31;
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= width) return;
-    const u64 tm = (j == width - 1) ? tail_mask(cols) : ~0ULL;
-    const u64 *s = src + (int64_t)blockIdx.z * sstride;
-    uint8_t *d = dst + (int64_t)blockIdx.z * dstride;
-    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
-        const u64 x = s[r * sp + j] & tm;
-        uint8_t *drow = d + r * dp + j * 64;
+    const int64_t j0 = j - lane;  // first word of this warp
+    if (j0 >= width) return;
+    const u64 tm = (j == width - 1) ? tail_mask(a.cols) : ~0ULL;
+    const int64_t q = blockIdx.z;
+    const int64_t p = a.fuse ? q / 7 : q;
+    const unsigned mask = a.fuse ? a.mask[q % 7] : 1u;
+    const u64 *s = a.src + p * a.sstride + j;
+    uint8_t *d = a.dst + q * a.dstride + j0 * 64;
+    const int64_t nbytes = min((int64_t)2048, a.dp - j0 * 64);  // bytes this warp owns in a row
+    for (int64_t r = blockIdx.y; r < a.rows; r += gridDim.y) {
+        u64 x = 0;
+        if (j < width) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            if (j * 64 + c * 16 >= dp) break;
-            const uint32_t h16 = (uint32_t)(x >> (48 - 16 * c)) & 0xFFFFu;
+            for (int t = 0; t < 4; ++t)
+                if (mask & (1u << t)) x ^= __ldg(s + a.qoff[t] + r * a.sp);
+            x &= tm;
+        }
+        uint8_t *drow = d + r * a.dp;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int ci = lane + 32 * k;  // 16-byte chunk within the warp's 2 KiB
+            const u64 xv = __shfl_sync(0xffffffffu, x, ci >> 2);
+            if (ci * 16 >= nbytes) continue;
+            const int c = ci & 3;
+            const uint32_t h16 = (uint32_t)(xv >> (48 - 16 * c)) & 0xFFFFu;
             const uint32_t rv = __brev(h16) >> 16;  // entry 16c+i at bit i
             uint4 v;
-            v.x = (((rv >> 0) & 0xF) * 0x00204081u & 0x01010101u) * one;
-            v.y = (((rv >> 4) & 0xF) * 0x00204081u & 0x01010101u) * one;
-            v.z = (((rv >> 8) & 0xF) * 0x00204081u & 0x01010101u) * one;
-            v.w = (((rv >> 12) & 0xF) * 0x00204081u & 0x01010101u) * one;
-            *reinterpret_cast<uint4 *>(drow + c * 16) = v;
+            v.x = (((rv >> 0) & 0xF) * 0x00204081u & 0x01010101u) * a.one;
+            v.y = (((rv >> 4) & 0xF) * 0x00204081u & 0x01010101u) * a.one;
+            v.z = (((rv >> 8) & 0xF) * 0x00204081u & 0x01010101u) * a.one;
+            v.w = (((rv >> 12) & 0xF) * 0x00204081u & 0x01010101u) * a.one;
+            *reinterpret_cast<uint4 *>(drow + ci * 16) = v;
         }
     }
 }
@@ -147,6 +178,12 @@ struct UArgs {
     int mt, nt, kblocks, kchunk_blocks, nchunks;
     int64_t nprob;
     int mode;  // 0 store, 1 xor, 2 atomic xor
+    // last Strassen level's post-addition fused into the epilogue: product
+    // q = 7p + i is XORed (red.global.xor) into the quadrants post_mask[i] of
+    // the level-(d-1) product p at C + p*sc + qoffC[Q] (C pre-zeroed).
+    int post;
+    int64_t qoffC[4];
+    unsigned post_mask[7];
 };
 
 template <int KIND>
@@ -284,7 +321,22 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
             tc_fence_before();
             mbar_arrive(bar_tempty + 8 * acc);
             const int64_t row = (int64_t)mtile * BM + q * 32 + lane;
-            if (row < p.m) {
+            if (p.post && row < p.m) {
+                const unsigned dm = p.post_mask[prob % 7];
+                u64 *cbase = p.C + (int64_t)(prob / 7) * p.sc + row * p.pc;
+#pragma unroll
+                for (int Q = 0; Q < 4; ++Q) {
+                    if (!(dm & (1u << Q))) continue;
+                    u64 *crow = cbase + p.qoffC[Q];
+#pragma unroll
+                    for (int w = 0; w < BN / 64; ++w) {
+                        const int64_t wi = (int64_t)ntile * (BN / 64) + w;
+                        if (wi >= p.Wn) break;
+                        const u64 v = ((u64)packed[2 * w] << 32) | (u64)packed[2 * w + 1];
+                        if (v) atomicXor(reinterpret_cast<unsigned long long *>(crow + wi), (unsigned long long)v);
+                    }
+                }
+            } else if (row < p.m) {
                 u64 *crow = p.C + prob * p.sc + row * p.pc;
                 const u64 ctm = tail_mask(p.n);
 #pragma unroll
@@ -349,29 +401,32 @@ int g_sms = 0;
 
 }  // namespace
 
-int launch_expand(const u64 *src, int64_t sp, int64_t sstride, uint8_t *dst, int64_t dp, int64_t dstride,
-                  int64_t rows, int64_t cols, int64_t nprob, uint32_t one, cudaStream_t s) {
-    const int64_t width = words_per_row(cols);
-    if (!rows || !width || !nprob) return GF2_OK;
-    dim3 blk((unsigned)(width >= 128 ? 128 : (width >= 32 ? 32 : width)));
-    dim3 grd((unsigned)((width + blk.x - 1) / blk.x), (unsigned)(rows > 65535 ? 65535 : rows), (unsigned)nprob);
-    k_expand<<<grd, blk, 0, s>>>(src, sp, sstride, dst, dp, dstride, rows, cols, one);
+int launch_expand(const ExpandArgs &a, int64_t nprob, cudaStream_t s) {
+    const int64_t width = words_per_row(a.cols);
+    if (!a.rows || !width || !nprob) return GF2_OK;
+    dim3 blk((unsigned)(width >= 128 ? 128 : (width + 31) / 32 * 32));
+    dim3 grd((unsigned)((width + blk.x - 1) / blk.x), (unsigned)(a.rows > 65535 ? 65535 : a.rows),
+             (unsigned)nprob);
+    k_expand<<<grd, blk, 0, s>>>(a);
     note_launch();
     return check_cuda(cudaGetLastError(), "k_expand launch");
 }
 
-// C (^)= A.B for a batch of problems via byte expansion + tcgen05. kind: 0 i8, 1 f8.
-int launch_umma(const M4rmBatch &b, int kind, cudaStream_t s) {
-    if (!b.m || !b.n || !b.nprob) return GF2_OK;
-    if (b.l == 0) {
-        if (b.accumulate) return GF2_OK;
-        for (int64_t q = 0; q < b.nprob; ++q) {
-            gf2_view v{b.C + q * b.sc, b.pc, b.m, b.n};
+// The tensor-core product for a batch: C (^)= A.B per problem, byte expansion
+// (optionally fused with the last Strassen pre-addition) + tcgen05 GEMM
+// (optionally fused with the last post-addition). kind: 0 i8, 1 f8.
+int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
+    const int64_t nprob = jb.fuse_pre ? 7 * jb.nsrc : jb.nsrc;
+    if (!jb.m || !jb.n || !nprob) return GF2_OK;
+    if (nprob > 65535) return set_error(GF2_ERR_PARAMETER, "too many problems for the tensor-core path");
+    if (jb.l == 0) {
+        if (jb.accumulate || jb.fuse_post) return GF2_OK;
+        for (int64_t q = 0; q < nprob; ++q) {
+            gf2_view v{jb.C + q * jb.sc, jb.pc, jb.m, jb.n};
             GF2_TRY(launch_ewise(v, nullptr, nullptr, 0, s));
         }
         return GF2_OK;
     }
-    if (b.nprob > 65535) return set_error(GF2_ERR_PARAMETER, "too many problems for the tensor-core path");
     if (!g_sms) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -381,8 +436,8 @@ int launch_umma(const M4rmBatch &b, int kind, cudaStream_t s) {
         GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES),
                            "umma smem attr"));
     }
-    const int64_t kp = (b.l + 15) / 16 * 16, np = (b.n + 15) / 16 * 16;
-    const int64_t a_bytes = b.nprob * b.m * kp, b_bytes = b.nprob * b.l * np;
+    const int64_t kp = (jb.l + 15) / 16 * 16, np = (jb.n + 15) / 16 * 16;
+    const int64_t a_bytes = nprob * jb.m * kp, b_bytes = nprob * jb.l * np;
     uint8_t *ws = nullptr;
     cudaError_t e = cudaMallocAsync((void **)&ws, (size_t)(a_bytes + b_bytes), s);
     if (e != cudaSuccess) {
@@ -391,38 +446,59 @@ int launch_umma(const M4rmBatch &b, int kind, cudaStream_t s) {
     }
     uint8_t *a8 = ws, *b8 = ws + a_bytes;
     const uint32_t one = kind == 0 ? 0x01u : 0x38u;
-    int rc = launch_expand(b.A, b.pa, b.sa, a8, kp, b.m * kp, b.m, b.l, b.nprob, one, s);
-    if (rc == GF2_OK) rc = launch_expand(b.B, b.pb, b.sb, b8, np, b.l * np, b.l, b.n, b.nprob, one, s);
+    // A side (rows m, cols l) and B side (rows l, cols n), quadrant offsets
+    // of the level-(d-1) source problems when fused
+    ExpandArgs ea{};
+    ea.src = jb.A; ea.sp = jb.pa; ea.sstride = jb.sa; ea.fuse = jb.fuse_pre;
+    ea.qoff[0] = 0; ea.qoff[1] = jb.l / 64; ea.qoff[2] = jb.m * jb.pa; ea.qoff[3] = jb.m * jb.pa + jb.l / 64;
+    for (int i = 0; i < 7; ++i) ea.mask[i] = jb.maskA[i];
+    ea.dst = a8; ea.dp = kp; ea.dstride = jb.m * kp; ea.rows = jb.m; ea.cols = jb.l; ea.one = one;
+    ExpandArgs eb{};
+    eb.src = jb.B; eb.sp = jb.pb; eb.sstride = jb.sb; eb.fuse = jb.fuse_pre;
+    eb.qoff[0] = 0; eb.qoff[1] = jb.n / 64; eb.qoff[2] = jb.l * jb.pb; eb.qoff[3] = jb.l * jb.pb + jb.n / 64;
+    for (int i = 0; i < 7; ++i) eb.mask[i] = jb.maskB[i];
+    eb.dst = b8; eb.dp = np; eb.dstride = jb.l * np; eb.rows = jb.l; eb.cols = jb.n; eb.one = one;
+    int rc = launch_expand(ea, nprob, s);
+    if (rc == GF2_OK) rc = launch_expand(eb, nprob, s);
     CUtensorMap ta, tb;
-    if (rc == GF2_OK) rc = make_map(&ta, a8, (uint64_t)b.l, (uint64_t)b.m, (uint64_t)b.nprob, kp, b.m * kp);
-    if (rc == GF2_OK) rc = make_map(&tb, b8, (uint64_t)b.n, (uint64_t)b.l, (uint64_t)b.nprob, np, b.l * np);
+    if (rc == GF2_OK) rc = make_map(&ta, a8, (uint64_t)jb.l, (uint64_t)jb.m, (uint64_t)nprob, kp, jb.m * kp);
+    if (rc == GF2_OK) rc = make_map(&tb, b8, (uint64_t)jb.n, (uint64_t)jb.l, (uint64_t)nprob, np, jb.l * np);
     if (rc == GF2_OK) {
         UArgs ua{};
-        ua.C = b.C;
-        ua.pc = b.pc;
-        ua.sc = b.sc;
-        ua.m = b.m;
-        ua.n = b.n;
-        ua.Wn = words_per_row(b.n);
-        ua.mt = (int)((b.m + BM - 1) / BM);
-        ua.nt = (int)((b.n + BN - 1) / BN);
-        ua.kblocks = (int)((b.l + BK - 1) / BK);
+        ua.C = jb.C;
+        ua.pc = jb.pc;
+        ua.sc = jb.sc;
+        ua.m = jb.m;
+        ua.n = jb.n;
+        ua.Wn = words_per_row(jb.n);
+        ua.mt = (int)((jb.m + BM - 1) / BM);
+        ua.nt = (int)((jb.n + BN - 1) / BN);
+        ua.kblocks = (int)((jb.l + BK - 1) / BK);
         ua.kchunk_blocks = kind == 0 ? ua.kblocks : (int)(F8_KCHUNK / BK);
         ua.nchunks = (ua.kblocks + ua.kchunk_blocks - 1) / ua.kchunk_blocks;
-        ua.nprob = b.nprob;
-        if (ua.nchunks > 1) {
-            if (!b.accumulate) {
-                for (int64_t q = 0; q < b.nprob && rc == GF2_OK; ++q) {
-                    gf2_view v{b.C + q * b.sc, b.pc, b.m, b.n};
+        ua.nprob = nprob;
+        ua.post = jb.fuse_post;
+        if (jb.fuse_post) {
+            ua.qoffC[0] = 0;
+            ua.qoffC[1] = jb.n / 64;
+            ua.qoffC[2] = jb.m * jb.pc;
+            ua.qoffC[3] = jb.m * jb.pc + jb.n / 64;
+            for (int i = 0; i < 7; ++i) ua.post_mask[i] = jb.maskC[i];
+            ua.mode = 2;  // destinations pre-zeroed (or accumulated into) by the caller
+        } else if (ua.nchunks > 1) {
+            if (!jb.accumulate) {
+                for (int64_t q = 0; q < nprob && rc == GF2_OK; ++q) {
+                    gf2_view v{jb.C + q * jb.sc, jb.pc, jb.m, jb.n};
                     rc = launch_ewise(v, nullptr, nullptr, 0, s);
                 }
             }
             ua.mode = 2;
         } else {
-            ua.mode = b.accumulate ? 1 : 0;
+            ua.mode = jb.accumulate ? 1 : 0;
         }
-        const int64_t ntiles = (int64_t)ua.nchunks * b.nprob * ua.mt * ua.nt;
+        const int64_t ntiles = (int64_t)ua.nchunks * nprob * ua.mt * ua.nt;
         const int grid = (int)(ntiles < g_sms ? ntiles : g_sms);
+        const int tidx = rc == GF2_OK ? timer_begin(s, (double)jb.m * (double)jb.l * (double)jb.n * (double)nprob) : -1;
         if (rc == GF2_OK) {
             if (kind == 0)
                 k_umma<0><<<grid, UMMA_THREADS, SMEM_BYTES, s>>>(ta, tb, ua);
@@ -431,9 +507,20 @@ int launch_umma(const M4rmBatch &b, int kind, cudaStream_t s) {
             note_launch();
             rc = check_cuda(cudaGetLastError(), "k_umma launch");
         }
+        timer_end(tidx, s);
     }
     cudaFreeAsync(ws, s);
     return rc;
+}
+
+int launch_umma(const M4rmBatch &b, int kind, cudaStream_t s) {
+    UmmaJob jb{};
+    jb.A = b.A; jb.pa = b.pa; jb.sa = b.sa;
+    jb.B = b.B; jb.pb = b.pb; jb.sb = b.sb;
+    jb.C = b.C; jb.pc = b.pc; jb.sc = b.sc;
+    jb.m = b.m; jb.l = b.l; jb.n = b.n; jb.nsrc = b.nprob;
+    jb.accumulate = b.accumulate;
+    return launch_umma_job(jb, kind, s);
 }
 
 }  // namespace gf2

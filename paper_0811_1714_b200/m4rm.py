@@ -54,7 +54,7 @@ def _mul_into(c: Mat, a: Mat, b: Mat, k: int, accumulate: bool) -> None:
 def mul_m4rm(a: Mat, b: Mat, k: int) -> BitMatrix:
     """m4rm.py:124-129 -- basic Four-Russians product."""
     _validate(a, b, k, 1, 1)
-    c = create(a.nrows, b.ncols, a.device)
+    c = BitMatrix(a.nrows, b.ncols, a.device, _overwritten=True)
     _mul_into(c, a, b, k, False)
     return c
 
@@ -62,7 +62,7 @@ def mul_m4rm(a: Mat, b: Mat, k: int) -> BitMatrix:
 def mul_m4rm_blocked(a: Mat, b: Mat, k: int, b_s: int) -> BitMatrix:
     """m4rm.py:132-137"""
     _validate(a, b, k, 1, b_s)
-    c = create(a.nrows, b.ncols, a.device)
+    c = BitMatrix(a.nrows, b.ncols, a.device, _overwritten=True)
     _mul_into(c, a, b, k, False)
     return c
 
@@ -71,7 +71,7 @@ def mul_m4rm_multitable(a: Mat, b: Mat, k: int, t: int,
                         b_s: int) -> BitMatrix:
     """m4rm.py:140-147"""
     _validate(a, b, k, t, b_s)
-    c = create(a.nrows, b.ncols, a.device)
+    c = BitMatrix(a.nrows, b.ncols, a.device, _overwritten=True)
     _mul_into(c, a, b, k, False)
     return c
 

@@ -89,7 +89,7 @@ def mul_strassen(a: Mat, b: Mat, params: MulParams | None = None) -> BitMatrix:
             f"inner dimensions {a.ncols} and {b.nrows} differ")
     if params is None:
         params = default_params()
-    c = create(a.nrows, b.ncols, a.device)
+    c = BitMatrix(a.nrows, b.ncols, a.device, _overwritten=a.ncols > 0)
     if a.nrows and b.ncols and a.ncols:
         _strassen(c, a, b, params, False)
     return c
@@ -108,3 +108,24 @@ def addmul(c: Mat, a: Mat, b: Mat, params: MulParams | None = None) -> None:
     if params is None:
         params = default_params()
     _strassen(c, a, b, params, True)
+
+
+def mul_direct(a: Mat, b: Mat) -> BitMatrix:
+    """One product launch with the current engine (set_engine), without the
+    Strassen recursion: the tensor-core contraction of north_star (c) when a
+    tcgen05 engine is selected, the M4RM kernel otherwise."""
+    if a.ncols != b.nrows:
+        raise DimensionError(
+            f"inner dimensions {a.ncols} and {b.nrows} differ")
+    c = BitMatrix(a.nrows, b.ncols, a.device, _overwritten=True)
+    _check_cuda_dev(c, a, b)
+    _lib.check(_lib.lib_cuda().gf2_mul(c._view(), a._view(), b._view(), 0,
+                                       _stream()))
+    return c
+
+
+def addmul_direct(c: Mat, a: Mat, b: Mat) -> None:
+    """C += A.B in one product launch with the current engine."""
+    _check_cuda_dev(c, a, b)
+    _lib.check(_lib.lib_cuda().gf2_mul(c._view(), a._view(), b._view(), 1,
+                                       _stream()))

@@ -10,7 +10,7 @@ from oracle import gf2_port as P
 pytestmark = pytest.mark.gpu
 g = pytest.importorskip("paper_0811_1714_b200")
 
-ENGINES = ["tc-i8", "tc-f8"]
+ENGINES = ["m4rm", "tc-i8", "tc-f8"]
 
 
 @pytest.fixture(autouse=True)
@@ -34,7 +34,7 @@ def test_small_and_ragged(engine):
         m, l, n = (int(x) for x in rng.integers(1, 700, 3))
         a, b = g.random(m, l, trial + 1), g.random(l, n, trial + 2)
         want = O.naive_product(O.random(m, l, trial + 1), O.random(l, n, trial + 2))
-        c = g.mul_m4rm(a, b, 8)
+        c = g.mul_direct(a, b)
         assert np.array_equal(words(c), want.words), (engine, m, l, n)
         assert g.trailing_bits_clean(c)
 
@@ -44,18 +44,18 @@ def test_golden_and_windows(engine, golden):
     g.set_engine(engine)
     for i, m, l, n, sa, sb in golden["prod_cases"].tolist():
         a, b = g.random(m, l, sa), g.random(l, n, sb)
-        assert np.array_equal(words(g.mul_m4rm(a, b, 8)), golden[f"prod_{i}"])
+        assert np.array_equal(words(g.mul_direct(a, b)), golden[f"prod_{i}"])
         assert np.array_equal(words(g.mul_strassen(a, b, g.MulParams(cutoff=64))),
                               golden[f"prod_{i}"])
     pa, pb = g.random(90, 640, 77), g.random(700, 512, 78)
     aw = g.window(pa, 5, 64, 70, 385)
     bw = g.window(pb, 11, 192, 385, 250)
-    assert np.array_equal(words(g.mul_m4rm(aw, bw, 8)), golden["win_product"])
+    assert np.array_equal(words(g.mul_direct(aw, bw)), golden["win_product"])
     pc = g.random(80, 512, 79)
     g.addmul(g.window(pc, 3, 64, 70, 250), aw, bw, g.MulParams(cutoff=64))
     assert np.array_equal(words(pc), golden["win_accum_parent"])
     a, b, c = g.random(150, 333, 91), g.random(333, 200, 92), g.random(150, 200, 93)
-    g.mul_m4rm_into(c, a, b, 8, 64, 4)
+    g.addmul_direct(c, a, b)
     assert np.array_equal(words(c), golden["into_result"])
 
 
@@ -73,7 +73,7 @@ def test_adversarial_large_sums(engine):
         dense_b[5, ::3] = 0
         b = g.from_dense(dense_b)
         want = dense_b.sum(0) & 1
-        got = g.to_dense(g.mul_m4rm(a, b, 8))
+        got = g.to_dense(g.mul_direct(a, b))
         assert np.array_equal(got, np.tile(want, (128, 1))), (engine, l)
 
 
@@ -81,12 +81,12 @@ def test_adversarial_large_sums(engine):
 def test_configs(engine, digests):
     g.set_engine(engine)
     a, b = g.random(1024, 1024, 11), g.random(1024, 1024, 12)
-    assert O.digest(words(g.mul_m4rm(a, b, 8))) == digests["cfg1"]
+    assert O.digest(words(g.mul_direct(a, b))) == digests["cfg1"]
     a, b = g.random(4096, 4096, 21), g.random(4096, 4096, 22)
     assert O.digest(words(g.mul_strassen(a, b, g.MulParams(cutoff=1024, k=8)))) == digests["cfg2"]
     a, b = g.random(16384, 16384, 31), g.random(16384, 16384, 32)
     assert O.digest(words(g.mul_strassen(a, b))) == digests["cfg3"]
-    assert O.digest(words(g.mul_m4rm(a, b, 8))) == digests["cfg3"]
+    assert O.digest(words(g.mul_direct(a, b))) == digests["cfg3"]
     t = O.bernoulli_threshold(0.1)
     a = g.bernoulli(10000, 7001, 41, threshold=t)
     b = g.bernoulli(7001, 12345, 42, threshold=t)
@@ -101,3 +101,13 @@ def test_engine_switch_validation():
         g.set_engine("nope")
     g.set_engine("tc-f8")
     assert g.get_engine() == "tc-f8"
+
+
+def test_mul_m4rm_always_runs_m4rm():
+    g.set_engine("tc-i8")
+    a, b = g.random(200, 300, 1), g.random(300, 100, 2)
+    g._lib.timer_enable(True)
+    g.mul_m4rm(a, b, 8)
+    ms, ops, n = g._lib.timer_read()
+    g._lib.timer_enable(False)
+    assert n == 1 and ops == 200 * 300 * 100
