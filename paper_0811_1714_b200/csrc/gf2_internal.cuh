@@ -94,8 +94,9 @@ struct UmmaJob {
     u64 *C;
     int64_t pc, sc;
     int64_t m, l, n;  // product (leaf) dimensions
-    int64_t nsrc;     // source problems (x7 products when fuse_pre)
-    int fuse_pre, fuse_post, accumulate;
+    int64_t nsrc;     // source problems (x7^fuse_pre products)
+    int fuse_pre;     // Strassen levels fused into the expansion: 0, 1 or 2
+    int fuse_post, accumulate;
     unsigned maskA[7], maskB[7], maskC[7];
 };
 int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s);

@@ -24,6 +24,8 @@
 //   P7 = (A11+A21).(B12+B22)         -> C21 C22
 // HBM is plentiful (180 GB), so every level's operands get their own
 // buffers (stream-ordered pool) and the 7^d leaf products run concurrently.
+#include <stdlib.h>
+
 #include "gf2_internal.cuh"
 
 namespace gf2 {
@@ -74,13 +76,20 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
         Nw[i] = N[i] / kWordBits;
         P[i] = i == 0 ? 1 : P[i - 1] * 7;
     }
-    const int last = depth - 1;  // deepest materialized level
+    const int last = depth - 1;               // deepest materialized C level
+    // pre-addition levels fused into the expansion (GF2_FUSE_LEVELS=2 folds
+    // two levels into it; one is faster on B200)
+    static const int fuse_env = getenv("GF2_FUSE_LEVELS") ? atoi(getenv("GF2_FUSE_LEVELS")) : 1;
+    const int fp = (depth >= 2 && fuse_env >= 2) ? 2 : 1;
+    const int lastA = depth - fp;             // deepest materialized A/B level
     int64_t offA[24], offB[24], offC[24], total = 0;
     for (int i = 1; i <= last; ++i) {
-        offA[i] = total;
-        total += P[i] * M[i] * Lw[i];
-        offB[i] = total;
-        total += P[i] * L[i] * Nw[i];
+        if (i <= lastA) {
+            offA[i] = total;
+            total += P[i] * M[i] * Lw[i];
+            offB[i] = total;
+            total += P[i] * L[i] * Nw[i];
+        }
         offC[i] = total;
         total += P[i] * M[i] * Nw[i];
     }
@@ -94,7 +103,7 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
         }
     }
     int rc = GF2_OK;
-    for (int lv = 0; lv < last && rc == GF2_OK; ++lv) {
+    for (int lv = 0; lv < lastA && rc == GF2_OK; ++lv) {
         for (int side = 0; side < 2 && rc == GF2_OK; ++side) {
             CombineArgs c{};
             const bool isA = side == 0;
@@ -127,21 +136,24 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
     }
     if (rc == GF2_OK) {
         UmmaJob jb{};
-        if (last == 0) {
+        if (lastA == 0) {
             jb.A = A0.data; jb.pa = A0.pitch;
             jb.B = B0.data; jb.pb = B0.pitch;
+        } else {
+            jb.A = ws + offA[lastA]; jb.pa = Lw[lastA]; jb.sa = M[lastA] * Lw[lastA];
+            jb.B = ws + offB[lastA]; jb.pb = Nw[lastA]; jb.sb = L[lastA] * Nw[lastA];
+        }
+        if (last == 0) {
             jb.C = C0.data; jb.pc = C0.pitch;
             if (!accumulate) rc = launch_ewise(C0, nullptr, nullptr, 0, s);
         } else {
-            jb.A = ws + offA[last]; jb.pa = Lw[last]; jb.sa = M[last] * Lw[last];
-            jb.B = ws + offB[last]; jb.pb = Nw[last]; jb.sb = L[last] * Nw[last];
             jb.C = ws + offC[last]; jb.pc = Nw[last]; jb.sc = M[last] * Nw[last];
             rc = check_cuda(cudaMemsetAsync(ws + offC[last], 0, (size_t)(P[last] * M[last] * Nw[last]) * 8, s),
                             "zero C_{d-1}");
         }
         jb.m = M[depth]; jb.l = L[depth]; jb.n = N[depth];
-        jb.nsrc = P[last];
-        jb.fuse_pre = 1;
+        jb.nsrc = P[lastA];
+        jb.fuse_pre = fp;
         jb.fuse_post = 1;
         for (int i = 0; i < 7; ++i) {
             jb.maskA[i] = kSA[i];

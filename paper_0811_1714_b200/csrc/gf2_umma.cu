@@ -21,6 +21,7 @@
 //   (red.global.xor), far inside the 2^24 f32 integer range.
 #include <cuda.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "gf2_internal.cuh"
@@ -118,9 +119,11 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
 struct ExpandArgs {
     const u64 *src;
     int64_t sp, sstride;
-    int64_t qoff[4];
+    int64_t qoff[4];   // quadrant offsets, first fused level (2x leaf size when levels == 2)
+    int64_t qoff2[4];  // quadrant offsets, second fused level (leaf size)
     unsigned mask[7];
-    int fuse;
+    int levels;        // fused Strassen levels: 0, 1 (q = 7p+i) or 2 (q = 49p+7i+j)
+    int64_t q0;        // first problem of this chunk (dst is indexed chunk-locally)
     uint8_t *dst;
     int64_t dp, dstride;
     int64_t rows, cols;
@@ -129,7 +132,46 @@ struct ExpandArgs {
 
 // A warp expands 32 consecutive words (2 KiB of bytes): every lane loads one
 // word, then the 128 16-byte chunks are written lane-contiguously (512 B per
-// store instruction) with the source word fetched by shuffle.
+// store instruction) with the source word fetched by shuffle. LEVELS = fused
+// Strassen levels (0, 1, 2): up to 1, 4 or 16 source blocks XORed per word,
+// all gathers issued before use; two rows per iteration for more MLP.
+template <int LEVELS>
+__device__ __forceinline__ u64 gather_word(const ExpandArgs &a, const u64 *s, int64_t r, unsigned m1,
+                                           unsigned m2) {
+    u64 x = 0;
+    if (LEVELS == 0) {
+        x = __ldg(s + r * a.sp);
+    } else if (LEVELS == 1) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (m1 & (1u << t)) x ^= __ldg(s + a.qoff[t] + r * a.sp);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if ((m1 >> (k >> 2)) & (m2 >> (k & 3)) & 1u) x ^= __ldg(s + a.qoff[k >> 2] + a.qoff2[k & 3] + r * a.sp);
+    }
+    return x;
+}
+
+__device__ __forceinline__ void expand_store(const ExpandArgs &a, uint8_t *drow, u64 x, int lane, int64_t nbytes) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int ci = lane + 32 * k;  // 16-byte chunk within the warp's 2 KiB
+        const u64 xv = __shfl_sync(0xffffffffu, x, ci >> 2);
+        if (ci * 16 >= nbytes) continue;
+        const int c = ci & 3;
+        const uint32_t h16 = (uint32_t)(xv >> (48 - 16 * c)) & 0xFFFFu;
+        const uint32_t rv = __brev(h16) >> 16;  // entry 16c+i at bit i
+        uint4 v;
+        v.x = (((rv >> 0) & 0xF) * 0x00204081u & 0x01010101u) * a.one;
+        v.y = (((rv >> 4) & 0xF) * 0x00204081u & 0x01010101u) * a.one;
+        v.z = (((rv >> 8) & 0xF) * 0x00204081u & 0x01010101u) * a.one;
+        v.w = (((rv >> 12) & 0xF) * 0x00204081u & 0x01010101u) * a.one;
+        *reinterpret_cast<uint4 *>(drow + ci * 16) = v;
+    }
+}
+
+template <int LEVELS>
 __global__ void k_expand(ExpandArgs a) {
     const int64_t width = words_per_row(a.cols);
     const int lane = threadIdx.x & 31;
@@ -137,36 +179,20 @@ __global__ void k_expand(ExpandArgs a) {
     const int64_t j0 = j - lane;  // first word of this warp
     if (j0 >= width) return;
     const u64 tm = (j == width - 1) ? tail_mask(a.cols) : ~0ULL;
-    const int64_t q = blockIdx.z;
-    const int64_t p = a.fuse ? q / 7 : q;
-    const unsigned mask = a.fuse ? a.mask[q % 7] : 1u;
+    const int64_t q = a.q0 + blockIdx.z;
+    const int64_t p = LEVELS == 0 ? q : (LEVELS == 1 ? q / 7 : q / 49);
+    const unsigned m1 = LEVELS == 0 ? 1u : a.mask[LEVELS == 1 ? q % 7 : (q / 7) % 7];
+    const unsigned m2 = LEVELS == 2 ? a.mask[q % 7] : 1u;
     const u64 *s = a.src + p * a.sstride + j;
-    uint8_t *d = a.dst + q * a.dstride + j0 * 64;
+    uint8_t *d = a.dst + (int64_t)blockIdx.z * a.dstride + j0 * 64;
     const int64_t nbytes = min((int64_t)2048, a.dp - j0 * 64);  // bytes this warp owns in a row
-    for (int64_t r = blockIdx.y; r < a.rows; r += gridDim.y) {
-        u64 x = 0;
-        if (j < width) {
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-                if (mask & (1u << t)) x ^= __ldg(s + a.qoff[t] + r * a.sp);
-            x &= tm;
-        }
-        uint8_t *drow = d + r * a.dp;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int ci = lane + 32 * k;  // 16-byte chunk within the warp's 2 KiB
-            const u64 xv = __shfl_sync(0xffffffffu, x, ci >> 2);
-            if (ci * 16 >= nbytes) continue;
-            const int c = ci & 3;
-            const uint32_t h16 = (uint32_t)(xv >> (48 - 16 * c)) & 0xFFFFu;
-            const uint32_t rv = __brev(h16) >> 16;  // entry 16c+i at bit i
-            uint4 v;
-            v.x = (((rv >> 0) & 0xF) * 0x00204081u & 0x01010101u) * a.one;
-            v.y = (((rv >> 4) & 0xF) * 0x00204081u & 0x01010101u) * a.one;
-            v.z = (((rv >> 8) & 0xF) * 0x00204081u & 0x01010101u) * a.one;
-            v.w = (((rv >> 12) & 0xF) * 0x00204081u & 0x01010101u) * a.one;
-            *reinterpret_cast<uint4 *>(drow + ci * 16) = v;
-        }
+    const bool live = j < width;
+    for (int64_t r = blockIdx.y; r < a.rows; r += 2 * (int64_t)gridDim.y) {
+        const int64_t r2 = r + gridDim.y;
+        const u64 x0 = live ? gather_word<LEVELS>(a, s, r, m1, m2) & tm : 0;
+        const u64 x1 = (live && r2 < a.rows) ? gather_word<LEVELS>(a, s, r2, m1, m2) & tm : 0;
+        expand_store(a, d + r * a.dp, x0, lane, nbytes);
+        if (r2 < a.rows) expand_store(a, d + r2 * a.dp, x1, lane, nbytes);
     }
 }
 
@@ -181,6 +207,7 @@ struct UArgs {
     // last Strassen level's post-addition fused into the epilogue: product
     // q = 7p + i is XORed (red.global.xor) into the quadrants post_mask[i] of
     // the level-(d-1) product p at C + p*sc + qoffC[Q] (C pre-zeroed).
+    int64_t q0;  // global index of this launch's problem 0 (C addressing)
     int post;
     int64_t qoffC[4];
     unsigned post_mask[7];
@@ -321,9 +348,10 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
             tc_fence_before();
             mbar_arrive(bar_tempty + 8 * acc);
             const int64_t row = (int64_t)mtile * BM + q * 32 + lane;
+            const int64_t gprob = p.q0 + prob;
             if (p.post && row < p.m) {
-                const unsigned dm = p.post_mask[prob % 7];
-                u64 *cbase = p.C + (int64_t)(prob / 7) * p.sc + row * p.pc;
+                const unsigned dm = p.post_mask[gprob % 7];
+                u64 *cbase = p.C + (gprob / 7) * p.sc + row * p.pc;
 #pragma unroll
                 for (int Q = 0; Q < 4; ++Q) {
                     if (!(dm & (1u << Q))) continue;
@@ -337,7 +365,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
                     }
                 }
             } else if (row < p.m) {
-                u64 *crow = p.C + prob * p.sc + row * p.pc;
+                u64 *crow = p.C + gprob * p.sc + row * p.pc;
                 const u64 ctm = tail_mask(p.n);
 #pragma unroll
                 for (int w = 0; w < BN / 64; ++w) {
@@ -405,9 +433,14 @@ int launch_expand(const ExpandArgs &a, int64_t nprob, cudaStream_t s) {
     const int64_t width = words_per_row(a.cols);
     if (!a.rows || !width || !nprob) return GF2_OK;
     dim3 blk((unsigned)(width >= 128 ? 128 : (width + 31) / 32 * 32));
-    dim3 grd((unsigned)((width + blk.x - 1) / blk.x), (unsigned)(a.rows > 65535 ? 65535 : a.rows),
+    dim3 grd((unsigned)((width + blk.x - 1) / blk.x), (unsigned)std::min<int64_t>(65535, (a.rows + 1) / 2),
              (unsigned)nprob);
-    k_expand<<<grd, blk, 0, s>>>(a);
+    if (a.levels == 0)
+        k_expand<0><<<grd, blk, 0, s>>>(a);
+    else if (a.levels == 1)
+        k_expand<1><<<grd, blk, 0, s>>>(a);
+    else
+        k_expand<2><<<grd, blk, 0, s>>>(a);
     note_launch();
     return check_cuda(cudaGetLastError(), "k_expand launch");
 }
@@ -416,7 +449,7 @@ int launch_expand(const ExpandArgs &a, int64_t nprob, cudaStream_t s) {
 // (optionally fused with the last Strassen pre-addition) + tcgen05 GEMM
 // (optionally fused with the last post-addition). kind: 0 i8, 1 f8.
 int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
-    const int64_t nprob = jb.fuse_pre ? 7 * jb.nsrc : jb.nsrc;
+    const int64_t nprob = jb.nsrc * (jb.fuse_pre == 2 ? 49 : (jb.fuse_pre == 1 ? 7 : 1));
     if (!jb.m || !jb.n || !nprob) return GF2_OK;
     if (nprob > 65535) return set_error(GF2_ERR_PARAMETER, "too many problems for the tensor-core path");
     if (jb.l == 0) {
@@ -437,76 +470,86 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
                            "umma smem attr"));
     }
     const int64_t kp = (jb.l + 15) / 16 * 16, np = (jb.n + 15) / 16 * 16;
-    const int64_t a_bytes = nprob * jb.m * kp, b_bytes = nprob * jb.l * np;
+    // byte operands for at most ~8 GiB of problems per launch (cfg5-sized
+    // recursions have thousands of leaves); chunks reuse one buffer
+    const int64_t per = jb.m * kp + jb.l * np;
+    const int64_t cap = (int64_t)8 << 30;
+    const int64_t qchunk = std::max<int64_t>(1, std::min<int64_t>(nprob, cap / std::max<int64_t>(per, 1)));
     uint8_t *ws = nullptr;
-    cudaError_t e = cudaMallocAsync((void **)&ws, (size_t)(a_bytes + b_bytes), s);
+    cudaError_t e = cudaMallocAsync((void **)&ws, (size_t)(qchunk * per), s);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return set_error(GF2_ERR_OOM, std::string("umma workspace: ") + cudaGetErrorString(e));
     }
-    uint8_t *a8 = ws, *b8 = ws + a_bytes;
+    uint8_t *a8 = ws, *b8 = ws + qchunk * jb.m * kp;
     const uint32_t one = kind == 0 ? 0x01u : 0x38u;
-    // A side (rows m, cols l) and B side (rows l, cols n), quadrant offsets
-    // of the level-(d-1) source problems when fused
+    // A side (rows m, cols l) and B side (rows l, cols n); quadrant offsets of
+    // the source problems for the fused Strassen levels
     ExpandArgs ea{};
-    ea.src = jb.A; ea.sp = jb.pa; ea.sstride = jb.sa; ea.fuse = jb.fuse_pre;
-    ea.qoff[0] = 0; ea.qoff[1] = jb.l / 64; ea.qoff[2] = jb.m * jb.pa; ea.qoff[3] = jb.m * jb.pa + jb.l / 64;
+    const int64_t f2 = jb.fuse_pre == 2 ? 2 : 1;  // first fused level's quadrants are f2 x leaf size
+    ea.src = jb.A; ea.sp = jb.pa; ea.sstride = jb.sa; ea.levels = jb.fuse_pre;
+    ea.qoff[0] = 0; ea.qoff[1] = f2 * jb.l / 64; ea.qoff[2] = f2 * jb.m * jb.pa; ea.qoff[3] = ea.qoff[1] + ea.qoff[2];
+    ea.qoff2[0] = 0; ea.qoff2[1] = jb.l / 64; ea.qoff2[2] = jb.m * jb.pa; ea.qoff2[3] = ea.qoff2[1] + ea.qoff2[2];
     for (int i = 0; i < 7; ++i) ea.mask[i] = jb.maskA[i];
     ea.dst = a8; ea.dp = kp; ea.dstride = jb.m * kp; ea.rows = jb.m; ea.cols = jb.l; ea.one = one;
     ExpandArgs eb{};
-    eb.src = jb.B; eb.sp = jb.pb; eb.sstride = jb.sb; eb.fuse = jb.fuse_pre;
-    eb.qoff[0] = 0; eb.qoff[1] = jb.n / 64; eb.qoff[2] = jb.l * jb.pb; eb.qoff[3] = jb.l * jb.pb + jb.n / 64;
+    eb.src = jb.B; eb.sp = jb.pb; eb.sstride = jb.sb; eb.levels = jb.fuse_pre;
+    eb.qoff[0] = 0; eb.qoff[1] = f2 * jb.n / 64; eb.qoff[2] = f2 * jb.l * jb.pb; eb.qoff[3] = eb.qoff[1] + eb.qoff[2];
+    eb.qoff2[0] = 0; eb.qoff2[1] = jb.n / 64; eb.qoff2[2] = jb.l * jb.pb; eb.qoff2[3] = eb.qoff2[1] + eb.qoff2[2];
     for (int i = 0; i < 7; ++i) eb.mask[i] = jb.maskB[i];
     eb.dst = b8; eb.dp = np; eb.dstride = jb.l * np; eb.rows = jb.l; eb.cols = jb.n; eb.one = one;
-    int rc = launch_expand(ea, nprob, s);
-    if (rc == GF2_OK) rc = launch_expand(eb, nprob, s);
-    CUtensorMap ta, tb;
-    if (rc == GF2_OK) rc = make_map(&ta, a8, (uint64_t)jb.l, (uint64_t)jb.m, (uint64_t)nprob, kp, jb.m * kp);
-    if (rc == GF2_OK) rc = make_map(&tb, b8, (uint64_t)jb.n, (uint64_t)jb.l, (uint64_t)nprob, np, jb.l * np);
-    if (rc == GF2_OK) {
-        UArgs ua{};
-        ua.C = jb.C;
-        ua.pc = jb.pc;
-        ua.sc = jb.sc;
-        ua.m = jb.m;
-        ua.n = jb.n;
-        ua.Wn = words_per_row(jb.n);
-        ua.mt = (int)((jb.m + BM - 1) / BM);
-        ua.nt = (int)((jb.n + BN - 1) / BN);
-        ua.kblocks = (int)((jb.l + BK - 1) / BK);
-        ua.kchunk_blocks = kind == 0 ? ua.kblocks : (int)(F8_KCHUNK / BK);
-        ua.nchunks = (ua.kblocks + ua.kchunk_blocks - 1) / ua.kchunk_blocks;
-        ua.nprob = nprob;
-        ua.post = jb.fuse_post;
-        if (jb.fuse_post) {
-            ua.qoffC[0] = 0;
-            ua.qoffC[1] = jb.n / 64;
-            ua.qoffC[2] = jb.m * jb.pc;
-            ua.qoffC[3] = jb.m * jb.pc + jb.n / 64;
-            for (int i = 0; i < 7; ++i) ua.post_mask[i] = jb.maskC[i];
-            ua.mode = 2;  // destinations pre-zeroed (or accumulated into) by the caller
-        } else if (ua.nchunks > 1) {
-            if (!jb.accumulate) {
-                for (int64_t q = 0; q < nprob && rc == GF2_OK; ++q) {
-                    gf2_view v{jb.C + q * jb.sc, jb.pc, jb.m, jb.n};
-                    rc = launch_ewise(v, nullptr, nullptr, 0, s);
-                }
+
+    UArgs ua{};
+    ua.C = jb.C;
+    ua.pc = jb.pc;
+    ua.sc = jb.sc;
+    ua.m = jb.m;
+    ua.n = jb.n;
+    ua.Wn = words_per_row(jb.n);
+    ua.mt = (int)((jb.m + BM - 1) / BM);
+    ua.nt = (int)((jb.n + BN - 1) / BN);
+    ua.kblocks = (int)((jb.l + BK - 1) / BK);
+    ua.kchunk_blocks = kind == 0 ? ua.kblocks : (int)(F8_KCHUNK / BK);
+    ua.nchunks = (ua.kblocks + ua.kchunk_blocks - 1) / ua.kchunk_blocks;
+    ua.post = jb.fuse_post;
+    int rc = GF2_OK;
+    if (jb.fuse_post) {
+        ua.qoffC[0] = 0;
+        ua.qoffC[1] = jb.n / 64;
+        ua.qoffC[2] = jb.m * jb.pc;
+        ua.qoffC[3] = jb.m * jb.pc + jb.n / 64;
+        for (int i = 0; i < 7; ++i) ua.post_mask[i] = jb.maskC[i];
+        ua.mode = 2;  // destinations pre-zeroed (or accumulated into) by the caller
+    } else if (ua.nchunks > 1) {
+        if (!jb.accumulate) {
+            for (int64_t q = 0; q < nprob && rc == GF2_OK; ++q) {
+                gf2_view v{jb.C + q * jb.sc, jb.pc, jb.m, jb.n};
+                rc = launch_ewise(v, nullptr, nullptr, 0, s);
             }
-            ua.mode = 2;
-        } else {
-            ua.mode = jb.accumulate ? 1 : 0;
         }
-        const int64_t ntiles = (int64_t)ua.nchunks * nprob * ua.mt * ua.nt;
+        ua.mode = 2;
+    } else {
+        ua.mode = jb.accumulate ? 1 : 0;
+    }
+    for (int64_t q0 = 0; q0 < nprob && rc == GF2_OK; q0 += qchunk) {
+        const int64_t nq = std::min<int64_t>(qchunk, nprob - q0);
+        ea.q0 = eb.q0 = ua.q0 = q0;
+        ua.nprob = nq;
+        rc = launch_expand(ea, nq, s);
+        if (rc == GF2_OK) rc = launch_expand(eb, nq, s);
+        CUtensorMap ta, tb;
+        if (rc == GF2_OK) rc = make_map(&ta, a8, (uint64_t)jb.l, (uint64_t)jb.m, (uint64_t)nq, kp, jb.m * kp);
+        if (rc == GF2_OK) rc = make_map(&tb, b8, (uint64_t)jb.n, (uint64_t)jb.l, (uint64_t)nq, np, jb.l * np);
+        if (rc != GF2_OK) break;
+        const int64_t ntiles = (int64_t)ua.nchunks * nq * ua.mt * ua.nt;
         const int grid = (int)(ntiles < g_sms ? ntiles : g_sms);
-        const int tidx = rc == GF2_OK ? timer_begin(s, (double)jb.m * (double)jb.l * (double)jb.n * (double)nprob) : -1;
-        if (rc == GF2_OK) {
-            if (kind == 0)
-                k_umma<0><<<grid, UMMA_THREADS, SMEM_BYTES, s>>>(ta, tb, ua);
-            else
-                k_umma<1><<<grid, UMMA_THREADS, SMEM_BYTES, s>>>(ta, tb, ua);
-            note_launch();
-            rc = check_cuda(cudaGetLastError(), "k_umma launch");
-        }
+        const int tidx = timer_begin(s, (double)jb.m * (double)jb.l * (double)jb.n * (double)nq);
+        if (kind == 0)
+            k_umma<0><<<grid, UMMA_THREADS, SMEM_BYTES, s>>>(ta, tb, ua);
+        else
+            k_umma<1><<<grid, UMMA_THREADS, SMEM_BYTES, s>>>(ta, tb, ua);
+        note_launch();
+        rc = check_cuda(cudaGetLastError(), "k_umma launch");
         timer_end(tidx, s);
     }
     cudaFreeAsync(ws, s);
