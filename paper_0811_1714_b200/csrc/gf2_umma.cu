@@ -21,6 +21,8 @@
 //   (red.global.xor), far inside the 2^24 f32 integer range.
 #include <cuda.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 #include <vector>
 
@@ -35,7 +37,6 @@ constexpr int STAGES = 4;
 constexpr int A_STAGE = BM * BK;          // 16 KiB
 constexpr int B_STAGE = BN * BK;          // 32 KiB
 constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
 constexpr int UMMA_THREADS = 256;
 constexpr int64_t F8_KCHUNK = 8192;
 
@@ -213,42 +214,163 @@ struct UArgs {
     unsigned post_mask[7];
 };
 
-template <int KIND>
+template <int CG>
+__device__ __forceinline__ void umma_commit_cg(uint32_t bar) {
+    if (CG == 1)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+                     : "memory");
+    else
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                bar),
+            "h"((uint16_t)3)
+            : "memory");
+}
+
+template <int KIND, int CG>
+__device__ __forceinline__ void umma_cg(uint32_t taddr, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    if (CG == 1) {
+        umma<KIND>(taddr, ad, bd, idesc, acc);
+    } else if (KIND == 0) {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(taddr),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+    } else {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(taddr),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+    }
+}
+
+// 2-SM TMA: each CTA loads its half into its own smem; the transaction bytes
+// land on the leader CTA's barrier (peer bit cleared).
+__device__ __forceinline__ void tma_load_3d_2sm(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                                uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3, %4}], [%5];\n" ::"r"(dst),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar & 0xFEFFFFFFu)
+        : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+
+// arrive on the leader CTA's copy of a barrier (cluster scope)
+__device__ __forceinline__ void mbar_arrive_leader(uint32_t bar) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(remote) : "r"(bar));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote) : "memory");
+}
+
+__device__ __forceinline__ void store_row(const UArgs &p, const uint32_t *packed, int64_t row, int ntile,
+                                          int64_t gprob) {
+    if (row >= p.m) return;
+    if (p.post) {
+        const unsigned dm = p.post_mask[gprob % 7];
+        u64 *cbase = p.C + (gprob / 7) * p.sc + row * p.pc;
+#pragma unroll
+        for (int Q = 0; Q < 4; ++Q) {
+            if (!(dm & (1u << Q))) continue;
+            u64 *crow = cbase + p.qoffC[Q];
+#pragma unroll
+            for (int w = 0; w < BN / 64; ++w) {
+                const int64_t wi = (int64_t)ntile * (BN / 64) + w;
+                if (wi >= p.Wn) break;
+                const u64 v = ((u64)packed[2 * w] << 32) | (u64)packed[2 * w + 1];
+                if (v) atomicXor(reinterpret_cast<unsigned long long *>(crow + wi), (unsigned long long)v);
+            }
+        }
+        return;
+    }
+    u64 *crow = p.C + gprob * p.sc + row * p.pc;
+    const u64 ctm = tail_mask(p.n);
+#pragma unroll
+    for (int w = 0; w < BN / 64; ++w) {
+        const int64_t wi = (int64_t)ntile * (BN / 64) + w;
+        if (wi >= p.Wn) break;
+        const u64 v = ((u64)packed[2 * w] << 32) | (u64)packed[2 * w + 1];
+        if (p.mode == 2) {
+            if (v) atomicXor(reinterpret_cast<unsigned long long *>(crow + wi), (unsigned long long)v);
+        } else if (p.mode == 1) {
+            crow[wi] ^= v;
+        } else if (wi == p.Wn - 1 && ctm != ~0ULL) {
+            crow[wi] = (crow[wi] & ~ctm) | v;
+        } else {
+            crow[wi] = v;
+        }
+    }
+}
+
+template <int CG>
+struct Geo {
+    static constexpr int MT = BM * CG;                   // rows per (pair) tile
+    static constexpr int A_ST = BM * BK;                 // 16 KiB per CTA
+    static constexpr int B_ST = (BN / CG) * BK;          // this CTA's N columns x BK
+    static constexpr int STG = CG == 1 ? 4 : 6;          // pipeline stages
+    static constexpr int SMEM = STG * (A_ST + B_ST) + 2048;
+};
+
+// CG = 1: one CTA, tile 128 x 256. CG = 2: a CTA pair (cluster of 2) with
+// tcgen05.mma.cta_group::2, tile 256 x 256; each CTA stages its 128 rows of A
+// and 128 of the 256 columns of B, so per-SM operand traffic drops by 1/3.
+template <int KIND, int CG>
 __global__ void __launch_bounds__(UMMA_THREADS, 1)
     k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, UArgs p) {
+    using G = Geo<CG>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    // 1024-byte alignment for the 128-byte swizzle atoms
-    const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;  // 128-byte swizzle atoms
     const uint32_t sA = base_u32;
-    const uint32_t sB = base_u32 + STAGES * A_STAGE;
-    const uint32_t sBar = sB + STAGES * B_STAGE;
-    const uint32_t bar_full = sBar, bar_empty = sBar + 8 * STAGES, bar_tfull = sBar + 16 * STAGES,
+    const uint32_t sB = base_u32 + G::STG * G::A_ST;
+    const uint32_t sBar = sB + G::STG * G::B_ST;
+    const uint32_t bar_full = sBar, bar_empty = sBar + 8 * G::STG, bar_tfull = sBar + 16 * G::STG,
                    bar_tempty = bar_tfull + 16;
     const uint32_t tmem_holder = bar_tempty + 16;
     unsigned char *gen_base = smem_raw + (base_u32 - smem_u32(smem_raw));
     volatile uint32_t *tmem_holder_ptr = reinterpret_cast<volatile uint32_t *>(gen_base + (tmem_holder - base_u32));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = CG == 1 ? 0u : cluster_rank();
+    const int64_t unit = CG == 1 ? blockIdx.x : (blockIdx.x >> 1);  // CTA or pair index
+    const int64_t nunits = CG == 1 ? gridDim.x : (gridDim.x >> 1);
     if (warp == 0 && lane == 0) {
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < G::STG; ++s) {
             mbar_init(bar_full + 8 * s, 1);
             mbar_init(bar_empty + 8 * s, 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(bar_tfull + 8 * b, 1);
-            mbar_init(bar_tempty + 8 * b, 128);
+            mbar_init(bar_tempty + 8 * b, 128 * CG);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(tmem_holder)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+        if (CG == 1) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(tmem_holder)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(tmem_holder)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+        }
     }
     tc_fence_before();
-    __syncthreads();
+    if (CG == 1)
+        __syncthreads();
+    else
+        cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder_ptr;
 
@@ -256,10 +378,10 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
     const int64_t ntiles = tiles_per_chunk * p.nchunks;
 
     if (warp == 0 && lane == 0) {
-        // ---------------- TMA producer
+        // ---------------- TMA producer (both CTAs of a pair)
         int stage = 0;
         uint32_t phase = 0;
-        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int64_t t = unit; t < ntiles; t += nunits) {
             const int chunk = (int)(t / tiles_per_chunk);
             int64_t r = t % tiles_per_chunk;
             const int prob = (int)(r / (p.mt * p.nt));
@@ -267,28 +389,35 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
             const int mtile = (int)(r / p.nt), ntile = (int)(r % p.nt);
             const int kb0 = chunk * p.kchunk_blocks;
             const int kb1 = min(kb0 + p.kchunk_blocks, p.kblocks);
+            const int arow = mtile * G::MT + (int)rank * BM;
             for (int kb = kb0; kb < kb1; ++kb) {
+                const uint32_t fb = bar_full + 8 * stage;
+                const uint32_t a_dst = sA + stage * G::A_ST, b_dst = sB + stage * G::B_ST;
                 mbar_wait(bar_empty + 8 * stage, phase ^ 1);
-                mbar_expect_tx(bar_full + 8 * stage, STAGE_BYTES);
-                tma_load_3d(sA + stage * A_STAGE, &tmA, kb * BK, mtile * BM, prob, bar_full + 8 * stage);
-                tma_load_3d(sB + stage * B_STAGE, &tmB, ntile * BN, kb * BK, prob, bar_full + 8 * stage);
-                tma_load_3d(sB + stage * B_STAGE + B_STAGE / 2, &tmB, ntile * BN + 128, kb * BK, prob,
-                            bar_full + 8 * stage);
-                if (++stage == STAGES) {
+                if (CG == 1) {
+                    mbar_expect_tx(fb, G::A_ST + G::B_ST);
+                    tma_load_3d(a_dst, &tmA, kb * BK, arow, prob, fb);
+                    tma_load_3d(b_dst, &tmB, ntile * BN, kb * BK, prob, fb);
+                    tma_load_3d(b_dst + G::B_ST / 2, &tmB, ntile * BN + 128, kb * BK, prob, fb);
+                } else {
+                    if (rank == 0) mbar_expect_tx(fb, 2 * (G::A_ST + G::B_ST));
+                    tma_load_3d_2sm(a_dst, &tmA, kb * BK, arow, prob, fb);
+                    tma_load_3d_2sm(b_dst, &tmB, ntile * BN + (int)rank * 128, kb * BK, prob, fb);
+                }
+                if (++stage == G::STG) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
         }
-    } else if (warp == 1 && lane == 0) {
-        // ---------------- MMA issuer
-        // instruction descriptor: D format, A/B formats, B MN-major, N, M
+    } else if (warp == 1 && lane == 0 && rank == 0) {
+        // ---------------- MMA issuer (leader CTA)
         const uint32_t idesc = (KIND == 0 ? (2u << 4) : (1u << 4)) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) |
-                               ((uint32_t)(BM >> 4) << 24);
+                               ((uint32_t)(G::MT >> 4) << 24);
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
-        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        for (int64_t t = unit; t < ntiles; t += nunits, ++it) {
             const int chunk = (int)(t / tiles_per_chunk);
             const int kb0 = chunk * p.kchunk_blocks;
             const int kb1 = min(kb0 + p.kchunk_blocks, p.kblocks);
@@ -302,23 +431,23 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
                 tc_fence_after();
 #pragma unroll
                 for (int k = 0; k < BK / 32; ++k) {
-                    const uint64_t ad = smem_desc(sA + stage * A_STAGE + k * 32, 16, 1024);
-                    const uint64_t bd = smem_desc(sB + stage * B_STAGE + k * 32 * 128, B_STAGE / 2, 1024);
-                    umma<KIND>(taddr, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                    const uint64_t ad = smem_desc(sA + stage * G::A_ST + k * 32, 16, 1024);
+                    const uint64_t bd = smem_desc(sB + stage * G::B_ST + k * 32 * 128, CG == 1 ? G::B_ST / 2 : 16, 1024);
+                    umma_cg<KIND, CG>(taddr, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
                 }
-                umma_commit(bar_empty + 8 * stage);
-                if (++stage == STAGES) {
+                umma_commit_cg<CG>(bar_empty + 8 * stage);
+                if (++stage == G::STG) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
-            umma_commit(bar_tfull + 8 * acc);
+            umma_commit_cg<CG>(bar_tfull + 8 * acc);
         }
     } else if (warp >= 4) {
-        // ---------------- epilogue: TMEM -> parity bits -> C
+        // ---------------- epilogue: TMEM -> parity bits -> C (each CTA its rows)
         const int q = warp & 3;  // TMEM lane quadrant
         int it = 0;
-        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        for (int64_t t = unit; t < ntiles; t += nunits, ++it) {
             int64_t r = t % tiles_per_chunk;
             const int prob = (int)(r / (p.mt * p.nt));
             r %= (p.mt * p.nt);
@@ -346,50 +475,25 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
                 packed[c] = pk;
             }
             tc_fence_before();
-            mbar_arrive(bar_tempty + 8 * acc);
-            const int64_t row = (int64_t)mtile * BM + q * 32 + lane;
-            const int64_t gprob = p.q0 + prob;
-            if (p.post && row < p.m) {
-                const unsigned dm = p.post_mask[gprob % 7];
-                u64 *cbase = p.C + (gprob / 7) * p.sc + row * p.pc;
-#pragma unroll
-                for (int Q = 0; Q < 4; ++Q) {
-                    if (!(dm & (1u << Q))) continue;
-                    u64 *crow = cbase + p.qoffC[Q];
-#pragma unroll
-                    for (int w = 0; w < BN / 64; ++w) {
-                        const int64_t wi = (int64_t)ntile * (BN / 64) + w;
-                        if (wi >= p.Wn) break;
-                        const u64 v = ((u64)packed[2 * w] << 32) | (u64)packed[2 * w + 1];
-                        if (v) atomicXor(reinterpret_cast<unsigned long long *>(crow + wi), (unsigned long long)v);
-                    }
-                }
-            } else if (row < p.m) {
-                u64 *crow = p.C + gprob * p.sc + row * p.pc;
-                const u64 ctm = tail_mask(p.n);
-#pragma unroll
-                for (int w = 0; w < BN / 64; ++w) {
-                    const int64_t wi = (int64_t)ntile * (BN / 64) + w;
-                    if (wi >= p.Wn) break;
-                    const u64 v = ((u64)packed[2 * w] << 32) | (u64)packed[2 * w + 1];
-                    if (p.mode == 2) {
-                        if (v) atomicXor(reinterpret_cast<unsigned long long *>(crow + wi), (unsigned long long)v);
-                    } else if (p.mode == 1) {
-                        crow[wi] ^= v;
-                    } else if (wi == p.Wn - 1 && ctm != ~0ULL) {
-                        crow[wi] = (crow[wi] & ~ctm) | v;
-                    } else {
-                        crow[wi] = v;
-                    }
-                }
-            }
+            if (CG == 1)
+                mbar_arrive(bar_tempty + 8 * acc);
+            else
+                mbar_arrive_leader(bar_tempty + 8 * acc);
+            const int64_t row = (int64_t)mtile * G::MT + (int64_t)rank * BM + q * 32 + lane;
+            store_row(p, packed, row, ntile, p.q0 + prob);
         }
     }
     tc_fence_before();
-    __syncthreads();
+    if (CG == 1)
+        __syncthreads();
+    else
+        cluster_sync();
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem_base) : "memory");
+        if (CG == 1)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem_base) : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem_base) : "memory");
     }
 }
 
@@ -464,10 +568,14 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES),
-                           "umma smem attr"));
-        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES),
-                           "umma smem attr"));
+        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                Geo<1>::SMEM), "umma smem attr"));
+        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                Geo<1>::SMEM), "umma smem attr"));
+        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                Geo<2>::SMEM), "umma smem attr"));
+        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                Geo<2>::SMEM), "umma smem attr"));
     }
     const int64_t kp = (jb.l + 15) / 16 * 16, np = (jb.n + 15) / 16 * 16;
     // byte operands for at most ~8 GiB of problems per launch (cfg5-sized
@@ -506,7 +614,9 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
     ua.m = jb.m;
     ua.n = jb.n;
     ua.Wn = words_per_row(jb.n);
-    ua.mt = (int)((jb.m + BM - 1) / BM);
+    // 2-SM (cta_group::2) pairs by default; GF2_UMMA_CG=1 selects single-CTA tiles
+    static const int cg = getenv("GF2_UMMA_CG") ? atoi(getenv("GF2_UMMA_CG")) : 2;
+    ua.mt = (int)((jb.m + BM * cg - 1) / (BM * cg));
     ua.nt = (int)((jb.n + BN - 1) / BN);
     ua.kblocks = (int)((jb.l + BK - 1) / BK);
     ua.kchunk_blocks = kind == 0 ? ua.kblocks : (int)(F8_KCHUNK / BK);
@@ -542,14 +652,34 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
         if (rc == GF2_OK) rc = make_map(&tb, b8, (uint64_t)jb.n, (uint64_t)jb.l, (uint64_t)nq, np, jb.l * np);
         if (rc != GF2_OK) break;
         const int64_t ntiles = (int64_t)ua.nchunks * nq * ua.mt * ua.nt;
-        const int grid = (int)(ntiles < g_sms ? ntiles : g_sms);
         const int tidx = timer_begin(s, (double)jb.m * (double)jb.l * (double)jb.n * (double)nq);
-        if (kind == 0)
-            k_umma<0><<<grid, UMMA_THREADS, SMEM_BYTES, s>>>(ta, tb, ua);
-        else
-            k_umma<1><<<grid, UMMA_THREADS, SMEM_BYTES, s>>>(ta, tb, ua);
+        if (cg == 1) {
+            const int grid = (int)(ntiles < g_sms ? ntiles : g_sms);
+            if (kind == 0)
+                k_umma<0, 1><<<grid, UMMA_THREADS, Geo<1>::SMEM, s>>>(ta, tb, ua);
+            else
+                k_umma<1, 1><<<grid, UMMA_THREADS, Geo<1>::SMEM, s>>>(ta, tb, ua);
+        } else {
+            const int64_t pairs = std::min<int64_t>(ntiles, g_sms / 2);
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3((unsigned)(2 * pairs));
+            cfg.blockDim = dim3(UMMA_THREADS);
+            cfg.dynamicSmemBytes = Geo<2>::SMEM;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            if (kind == 0)
+                rc = check_cuda(cudaLaunchKernelEx(&cfg, k_umma<0, 2>, ta, tb, ua), "k_umma 2sm launch");
+            else
+                rc = check_cuda(cudaLaunchKernelEx(&cfg, k_umma<1, 2>, ta, tb, ua), "k_umma 2sm launch");
+        }
         note_launch();
-        rc = check_cuda(cudaGetLastError(), "k_umma launch");
+        if (rc == GF2_OK) rc = check_cuda(cudaGetLastError(), "k_umma launch");
         timer_end(tidx, s);
     }
     cudaFreeAsync(ws, s);
