@@ -110,6 +110,21 @@ int gf2_mul(const gf2_view *c, const gf2_view *a, const gf2_view *b,
 int gf2_strassen(const gf2_view *c, const gf2_view *a, const gf2_view *b,
                  int64_t cutoff, int k, int accumulate, void *stream);
 
+/* core.py:374-376 `transpose`: out (a.ncols x a.nrows) = a^T (bit-matrix
+ * transpose, 64x64 blocks per warp). */
+int gf2_transpose(const gf2_view *out, const gf2_view *a, void *stream);
+
+/* cubic.py:76-102 `mul_cubic`: C (^)= A.B by AND + XOR-fold + parity against
+ * B^T -- the reference's narrow-B (n < 64) base case. */
+int gf2_cubic(const gf2_view *c, const gf2_view *a, const gf2_view *b,
+              int accumulate, void *stream);
+
+/* dst[:, col0 : col0 + src.ncols) = src for ANY column offset (not only
+ * multiples of 64), keeping every other bit of dst: the building block of
+ * core.py:344-358 `augment` with a ragged left operand. */
+int gf2_copy_cols(const gf2_view *dst, int64_t col0, const gf2_view *src,
+                  void *stream);
+
 /* strassen.py:66-84 `peel_split`: writes {m', l', n', depth}. Host only. */
 int gf2_peel_split(int64_t m, int64_t l, int64_t n, int64_t cutoff,
                    int64_t out4[4]);

@@ -19,9 +19,11 @@ from .errors import (AlignmentError, DimensionError, FormatError, GF2MatError,
                      ParameterError)
 from .m4rm import (StripeSpec, mul_m4rm, mul_m4rm_blocked, mul_m4rm_into,
                    mul_m4rm_multitable)
+from .gf2m import load, save
 from .strassen import (GPU_CUTOFF, MulParams, PeelSplit, addmul,
                        addmul_direct, default_params, mul_direct,
                        mul_strassen, peel_split)
+from .structure import augment, mul_cubic, stack, transpose
 
 __version__ = "0.1.0"
 
@@ -37,4 +39,5 @@ __all__ = [
     "mul_strassen", "peel_split", "random", "set_engine", "tail_mask",
     "to_dense",
     "to_numpy", "trailing_bits_clean", "window", "words_per_row", "zero_into",
+    "augment", "load", "mul_cubic", "save", "stack", "transpose",
 ]

@@ -211,6 +211,43 @@ int gf2_strassen(const gf2_view *c, const gf2_view *a, const gf2_view *b, int64_
     return strassen_mul(*c, *a, *b, cutoff, accumulate ? 1 : 0, (cudaStream_t)stream);
 }
 
+int gf2_transpose(const gf2_view *out, const gf2_view *a, void *stream) {
+    GF2_TRY(check_view(out, "out"));
+    GF2_TRY(check_view(a, "a"));
+    if (out->nrows != a->ncols || out->ncols != a->nrows)
+        return set_error(GF2_ERR_DIMENSION, "transpose target " + std::to_string(out->nrows) + "x" +
+                                                std::to_string(out->ncols) + " != " + std::to_string(a->ncols) +
+                                                "x" + std::to_string(a->nrows));
+    if (overlaps(*out, *a)) return set_error(GF2_ERR_PARAMETER, "transpose target aliases its source");
+    return launch_transpose(*out, *a, (cudaStream_t)stream);
+}
+
+int gf2_cubic(const gf2_view *c, const gf2_view *a, const gf2_view *b, int accumulate, void *stream) {
+    GF2_TRY(check_mul(c, a, b));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t m = a->nrows, l = a->ncols, n = b->ncols;
+    if (!m || !n) return GF2_OK;
+    if (!l) return accumulate ? GF2_OK : launch_ewise(*c, nullptr, nullptr, 0, s);
+    gf2_view bt{nullptr, words_per_row(l), n, l};
+    GF2_TRY(check_cuda(cudaMallocAsync((void **)&bt.data, (size_t)(n * bt.pitch) * 8, s), "cubic workspace"));
+    int rc = launch_transpose(bt, *b, s);
+    if (rc == GF2_OK) rc = launch_cubic(*c, *a, bt, accumulate ? 1 : 0, s);
+    cudaFreeAsync(bt.data, s);
+    return rc;
+}
+
+int gf2_copy_cols(const gf2_view *dst, int64_t col0, const gf2_view *src, void *stream) {
+    GF2_TRY(check_view(dst, "dst"));
+    GF2_TRY(check_view(src, "src"));
+    if (src->nrows != dst->nrows || col0 < 0 || col0 + src->ncols > dst->ncols)
+        return set_error(GF2_ERR_DIMENSION, "column copy of " + std::to_string(src->nrows) + "x" +
+                                                std::to_string(src->ncols) + " at column " + std::to_string(col0) +
+                                                " exceeds " + std::to_string(dst->nrows) + "x" +
+                                                std::to_string(dst->ncols));
+    if (overlaps(*dst, *src)) return set_error(GF2_ERR_PARAMETER, "column copy target aliases its source");
+    return launch_copy_cols(*dst, col0, *src, (cudaStream_t)stream);
+}
+
 int gf2_peel_split(int64_t m, int64_t l, int64_t n, int64_t cutoff, int64_t out4[4]) {
     if (!out4) return set_error(GF2_ERR_PARAMETER, "null output");
     peel_split(m, l, n, cutoff, out4);

@@ -68,6 +68,9 @@ struct CombineArgs {
     int accumulate;
 };
 int launch_combine(const CombineArgs &a, cudaStream_t s);
+int launch_transpose(const gf2_view &out, const gf2_view &in, cudaStream_t s);
+int launch_cubic(const gf2_view &c, const gf2_view &a, const gf2_view &bt, int accumulate, cudaStream_t s);
+int launch_copy_cols(const gf2_view &dst, int64_t c0, const gf2_view &src, cudaStream_t s);
 
 // Batched M4RM: problem q uses A + q*sa, B + q*sb, C + q*sc (same dims).
 struct M4rmBatch {

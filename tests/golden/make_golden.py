@@ -96,6 +96,39 @@ def main(big: bool):
     c = g.copy_out(c0)
     g.mul_m4rm_into(c, a, b, 8, 64, 4)
     out["into_result"] = c.words.copy()
+    # --- GF2M file bytes and load() error messages (core.py:443-484)
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        fp = os.path.join(td, "m.gf2m")
+        g.save(g.random(37, 200, 5), fp)
+        good = open(fp, "rb").read()
+        out["gf2m_37x200_s5"] = np.frombuffer(good, dtype=np.uint8).copy()
+        g.save(g.window(g.random(9, 300, 6), 2, 64, 5, 130), fp)
+        out["gf2m_window"] = np.frombuffer(open(fp, "rb").read(), dtype=np.uint8).copy()
+        bad = {"truncated": good[:10], "magic": b"GF3M" + good[4:],
+               "version": good[:4] + b"\x02" + good[5:], "length": good[:-8]}
+        dirty = bytearray(good)
+        width = 4
+        off = 21 + (3 * width + width - 1) * 8  # row 3, last word, lowest byte
+        dirty[off] |= 1
+        bad["dirty"] = bytes(dirty)
+        msgs = []
+        for name, data in bad.items():
+            open(fp, "wb").write(data)
+            try:
+                g.load(fp)
+                msgs.append((name, ""))
+            except g.FormatError as exc:
+                msgs.append((name, str(exc)))
+        out["gf2m_error_names"] = np.array([n for n, _ in msgs])
+        out["gf2m_error_msgs"] = np.array([m for _, m in msgs])
+    # --- structural ops (core.py:344-376) and mul_cubic (cubic.py:76-102)
+    a, b = g.random(70, 130, 61), g.random(70, 77, 62)
+    out["augment_ragged"] = g.augment(a, b).words.copy()
+    out["augment_aligned"] = g.augment(g.random(70, 128, 63), b).words.copy()
+    out["stack"] = g.stack(g.random(30, 130, 64), g.random(41, 130, 65)).words.copy()
+    out["transpose_70x130"] = g.transpose(a).words.copy()
+    out["cubic_200x300x57"] = g.mul_cubic(g.random(200, 300, 66), g.random(300, 57, 67)).words.copy()
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **out)
 
     # --- config digests (SURVEY.md §8(c) seed convention 10i+1/2/3)

@@ -64,3 +64,24 @@ def test_k_panels():
         assert all(k0 % 64 == 0 for k0, _ in ps)
         for (a0, a1), (b0, b1) in zip(ps, ps[1:]):
             assert a1 == b0
+
+
+def test_gf2m_load_errors_match_reference(golden, tmp_path):
+    """core.py:455-484 messages and byte offsets (no GPU needed: the file
+    is validated on the host before any upload)."""
+    from paper_0811_1714_b200 import FormatError, load
+    good = golden["gf2m_37x200_s5"].tobytes()
+    width = 4
+    dirty = bytearray(good)
+    dirty[21 + (3 * width + width - 1) * 8] |= 1
+    cases = {"truncated": good[:10], "magic": b"GF3M" + good[4:],
+             "version": good[:4] + b"\x02" + good[5:], "length": good[:-8],
+             "dirty": bytes(dirty)}
+    want = dict(zip(golden["gf2m_error_names"].tolist(),
+                    golden["gf2m_error_msgs"].tolist()))
+    fp = tmp_path / "bad.gf2m"
+    for name, data in cases.items():
+        fp.write_bytes(data)
+        with pytest.raises(FormatError) as exc:
+            load(fp)
+        assert str(exc.value) == want[name], name
