@@ -120,6 +120,7 @@ int gf2_alloc(int64_t nrows, int64_t ncols, gf2_view *out, void *stream) {
     void *p = nullptr;
     cudaStream_t s = (cudaStream_t)stream;
     if (bytes) {
+        GF2_TRY(pool_setup());
         GF2_TRY(check_cuda(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync"));
         GF2_TRY(check_cuda(cudaMemsetAsync(p, 0, bytes, s), "cudaMemsetAsync"));
     }
@@ -229,6 +230,7 @@ int gf2_cubic(const gf2_view *c, const gf2_view *a, const gf2_view *b, int accum
     if (!m || !n) return GF2_OK;
     if (!l) return accumulate ? GF2_OK : launch_ewise(*c, nullptr, nullptr, 0, s);
     gf2_view bt{nullptr, words_per_row(l), n, l};
+    GF2_TRY(pool_setup());
     GF2_TRY(check_cuda(cudaMallocAsync((void **)&bt.data, (size_t)(n * bt.pitch) * 8, s), "cubic workspace"));
     int rc = launch_transpose(bt, *b, s);
     if (rc == GF2_OK) rc = launch_cubic(*c, *a, bt, accumulate ? 1 : 0, s);
@@ -255,3 +257,23 @@ int gf2_peel_split(int64_t m, int64_t l, int64_t n, int64_t cutoff, int64_t out4
 }
 
 }  // extern "C"
+
+namespace gf2 {
+// Stream-ordered pool for every workspace the library allocates: keep freed
+// blocks cached so repeated calls never go back to cudaMalloc (process-wide,
+// per device, idempotent).
+int pool_setup() {
+    static bool configured[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && configured[dev]) return GF2_OK;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thresh = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh);
+    }
+    cudaGetLastError();
+    if (dev < 64) configured[dev] = true;
+    return GF2_OK;
+}
+}  // namespace gf2

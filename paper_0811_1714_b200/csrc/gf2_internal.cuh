@@ -68,6 +68,7 @@ struct CombineArgs {
     int accumulate;
 };
 int launch_combine(const CombineArgs &a, cudaStream_t s);
+int pool_setup();
 int launch_transpose(const gf2_view &out, const gf2_view &in, cudaStream_t s);
 int launch_cubic(const gf2_view &c, const gf2_view &a, const gf2_view &bt, int accumulate, cudaStream_t s);
 int launch_copy_cols(const gf2_view &dst, int64_t c0, const gf2_view &src, cudaStream_t s);
@@ -105,8 +106,14 @@ struct UmmaJob {
 int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s);
 // multiply engine for every product (gf2_set_engine): 0 M4RM, 1 tcgen05 i8, 2 tcgen05 f8
 extern int g_engine;
+// Products below ~2^34 bit-ops run faster on the M4RM kernel than through
+// byte expansion + tensor cores (fixed costs dominate; tools/bench_configs.py:
+// 1024^3 is 15 us on M4RM vs 113 us on tc-i8), so the automatic dispatch
+// (Strassen leaves, small non-recursive products) routes them there.
+constexpr double kTensorMinWork = 17179869184.0;  // 2^34
 inline int launch_product(const M4rmBatch &b, cudaStream_t s) {
-    if (g_engine == 0) return launch_m4rm(b, s);
+    const double work = (double)b.m * (double)b.l * (double)b.n * (double)b.nprob;
+    if (g_engine == 0 || work < kTensorMinWork) return launch_m4rm(b, s);
     return launch_umma(b, g_engine == 1 ? 0 : 1, s);
 }
 int timer_enable(int on);

@@ -37,21 +37,6 @@ constexpr unsigned kSB[7] = {1, 4, 8, 15, 3, 11, 10};
 // product bits: 1 << (i-1) for P_i
 constexpr unsigned kSC[4] = {0x03, 0x35, 0x69, 0x71};
 
-bool g_pool_configured = false;
-
-int pool_setup() {
-    if (g_pool_configured) return GF2_OK;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thresh = UINT64_MAX;  // keep freed blocks cached in the pool
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh);
-    }
-    cudaGetLastError();
-    g_pool_configured = true;
-    return GF2_OK;
-}
 
 int m4rm_view(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accumulate, cudaStream_t s) {
     M4rmBatch mb{a.data, a.pitch, 0, b.data, b.pitch, 0, c.data, c.pitch, 0,
@@ -194,7 +179,11 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
 
 int strassen_core(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0, int depth, int accumulate,
                   cudaStream_t s) {
-    if (g_engine != 0) return strassen_core_tc(C0, A0, B0, depth, accumulate, s);
+    if (g_engine != 0) {
+        double leaf = (double)(A0.nrows >> depth) * (double)(A0.ncols >> depth) * (double)(B0.ncols >> depth);
+        for (int i = 0; i < depth; ++i) leaf *= 7.0;
+        if (leaf >= kTensorMinWork) return strassen_core_tc(C0, A0, B0, depth, accumulate, s);
+    }
     int64_t M[24], L[24], N[24], Lw[24], Nw[24], P[24];
     for (int i = 0; i <= depth; ++i) {
         M[i] = A0.nrows >> i;
@@ -326,7 +315,9 @@ int m4rm_mul(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accumu
 
 // gf2_mul: one product launch with the current engine, no recursion
 int engine_mul(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accumulate, cudaStream_t s) {
-    return m4rm_view(c, a, b, accumulate, s);
+    M4rmBatch mb{a.data, a.pitch, 0, b.data, b.pitch, 0, c.data, c.pitch, 0, a.nrows, a.ncols, b.ncols, 1, accumulate};
+    if (g_engine == 0) return launch_m4rm(mb, s);
+    return launch_umma(mb, g_engine == 1 ? 0 : 1, s);  // explicit engine: no size heuristic
 }
 
 // strassen.py:257-282 dispatch (+ peel_fixup strassen.py:219-249).

@@ -584,6 +584,7 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
     const int64_t cap = (int64_t)8 << 30;
     const int64_t qchunk = std::max<int64_t>(1, std::min<int64_t>(nprob, cap / std::max<int64_t>(per, 1)));
     uint8_t *ws = nullptr;
+    GF2_TRY(pool_setup());
     cudaError_t e = cudaMallocAsync((void **)&ws, (size_t)(qchunk * per), s);
     if (e != cudaSuccess) {
         cudaGetLastError();
