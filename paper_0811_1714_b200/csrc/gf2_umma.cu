@@ -914,7 +914,7 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
                                                 Geo<2>::SMEM), "umma smem attr"));
     }
     // i8 with 2-SM pairs: operand tiles built in shared memory from the packed
-    // bits (k_umma_cv) -- no byte expansion pass (GF2_UMMA_CONV=0 disables)
+    // bits (k_umma_cv) -- no byte expansion pass
     // opt-in (GF2_UMMA_CONV=1): shared-memory-bandwidth bound today, see DESIGN.md §4.4
     static const bool conv = getenv("GF2_UMMA_CONV") && atoi(getenv("GF2_UMMA_CONV")) == 1;
     static const int cgc = getenv("GF2_UMMA_CG") ? atoi(getenv("GF2_UMMA_CG")) : 2;
