@@ -142,6 +142,49 @@ __global__ void k_combine(CombineArgs p, int64_t wblocks) {
     }
 }
 
+// One Winograd level in a single pass: each thread loads its NS source
+// vectors once (the 4 quadrants for the pre-additions, the 7 products for the
+// post-additions) and writes all NQ outputs, instead of k_combine's one
+// output per thread re-reading 1-4 sources (14 source reads per 7 outputs).
+// Same CombineArgs addressing; 16-byte vectors, ROWS rows per thread.
+template <int NS, int NQ, int ROWS>
+__global__ void k_combine_all(CombineArgs p, int64_t wblocks) {
+    const int64_t prob = blockIdx.x / wblocks;
+    const int64_t j = ((blockIdx.x % wblocks) * blockDim.x + threadIdx.x) * 2;
+    if (j >= p.W) return;
+    const u64 *sb = p.src + prob * p.src_stride + j;
+    u64 *db = p.dst + prob * p.dst_stride + j;
+    const int64_t rstep = (int64_t)gridDim.y * blockDim.y * ROWS;
+    for (int64_t r0 = ((int64_t)blockIdx.y * blockDim.y + threadIdx.y) * ROWS; r0 < p.R; r0 += rstep) {
+#pragma unroll
+        for (int rr = 0; rr < ROWS; ++rr) {
+            const int64_t r = r0 + rr;
+            if (r >= p.R) break;
+            ulonglong2 in[NS];
+#pragma unroll
+            for (int i = 0; i < NS; ++i)
+                in[i] = __ldg(reinterpret_cast<const ulonglong2 *>(sb + p.src_off[i] + r * p.src_pitch));
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                ulonglong2 v = make_ulonglong2(0, 0);
+#pragma unroll
+                for (int i = 0; i < NS; ++i)
+                    if (p.mask[q] & (1u << i)) {
+                        v.x ^= in[i].x;
+                        v.y ^= in[i].y;
+                    }
+                ulonglong2 *d = reinterpret_cast<ulonglong2 *>(db + p.dst_off[q] + r * p.dst_pitch);
+                if (p.accumulate) {
+                    const ulonglong2 o = *d;
+                    v.x ^= o.x;
+                    v.y ^= o.y;
+                }
+                *d = v;
+            }
+        }
+    }
+}
+
 inline dim3 row_grid(int64_t width, int64_t nrows, dim3 blk) {
     int64_t gx = (width + blk.x - 1) / blk.x;
     int64_t gy = (nrows + blk.y - 1) / blk.y;
@@ -212,6 +255,20 @@ int launch_combine(const CombineArgs &a, cudaStream_t s) {
     const int64_t gx = wblocks * a.nprob * a.nq;
     int64_t gy = (a.R + blk.y * ROWS - 1) / (blk.y * ROWS);
     if (gy > 65535) gy = 65535;
+    int64_t gy2 = (a.R + blk.y * 2 - 1) / (blk.y * 2);
+    if (gy2 > 65535) gy2 = 65535;
+    unsigned used = 0;
+    for (int q = 0; q < a.nq; ++q) used |= a.mask[q];
+    if (v2 && a.nq == 7 && used == 0xF) {
+        k_combine_all<4, 7, 2><<<dim3((unsigned)(wblocks * a.nprob), (unsigned)gy2, 1), blk, 0, s>>>(a, wblocks);
+        note_launch();
+        return check_cuda(cudaGetLastError(), "k_combine_all launch");
+    }
+    if (v2 && a.nq == 4 && used == 0x7F) {
+        k_combine_all<7, 4, 2><<<dim3((unsigned)(wblocks * a.nprob), (unsigned)gy2, 1), blk, 0, s>>>(a, wblocks);
+        note_launch();
+        return check_cuda(cudaGetLastError(), "k_combine_all launch");
+    }
     if (v2)
         k_combine<2, ROWS><<<dim3((unsigned)gx, (unsigned)gy, 1), blk, 0, s>>>(a, wblocks);
     else
