@@ -44,7 +44,7 @@ def parse():
     p.add_argument("--cutoff", type=int, default=0,
                    help="Strassen cutoff (0 = device default)")
     p.add_argument("--npanels", type=int, default=4)
-    p.add_argument("--engine", default="tc-i8", choices=["m4rm", "tc-i8", "tc-f8"],
+    p.add_argument("--engine", default="tc-f4", choices=["m4rm", "tc-i8", "tc-f8", "tc-f4"],
                    help="product engine (results are identical)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -396,15 +396,19 @@ def main():
                            f"{peaks.get('hbm_gbs')} GB/s never binds here",
         }
     elif kern_n:
-        # 0/1 bytes through tcgen05 kind::i8 / kind::f8f6f4: 2 ops per MAC
+        # 0/1 entries through tcgen05 (kind::i8 / kind::f8f6f4 bytes, or
+        # kind::mxf4 e2m1 nibbles): 2 ops per MAC, against the dense nominal
+        # peak of that operand width (B200_PROFILING.md; no measured 8/4-bit peak)
         ach = 2.0 * kern_ops / (kern_ms * 1e-3) / 1e12
-        peak = 4500.0   # dense 8-bit nominal, B200_PROFILING.md (no measured 8-bit peak)
+        f4 = args.engine == "tc-f4"
+        peak = 9000.0 if f4 else 4500.0
         roofline = {
-            "bound": "tensor", "kernel": "k_umma (batched Strassen leaves)",
+            "bound": "tensor",
+            "kernel": ("k_umma_f4" if f4 else "k_umma") + " (batched Strassen leaves)",
             "achieved": ach, "peak": peak, "unit": "TFLOP/s",
             "frac": ach / peak, "traffic": None,
-            "peak_source": "nominal dense fp8/int8 4.5 PFLOP/s (B200_PROFILING.md); "
-                           "MEASURED_PEAKS bf16 x2 = "
+            "peak_source": ("nominal dense fp4 9 PFLOP/s" if f4 else "nominal dense fp8/int8 4.5 PFLOP/s")
+                           + " (B200_PROFILING.md); MEASURED_PEAKS bf16 x2 = "
                            f"{2 * float(peaks.get('bf16_tflops', 0)):.0f} TFLOP/s",
         }
     if roofline is not None:
@@ -416,7 +420,7 @@ def main():
         tr = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tr):
             try:
-                key = "k_m4rm" if args.engine == "m4rm" else "k_umma"
+                key = {"m4rm": "k_m4rm", "tc-f4": "k_umma_f4"}.get(args.engine, "k_umma")
                 roofline["traffic"] = json.load(open(tr)).get(key)
             except Exception:
                 pass

@@ -148,12 +148,13 @@ def timer_read():
     return ms.value, ops.value, n.value
 
 
-ENGINES = {"m4rm": 0, "tc-i8": 1, "tc-f8": 2}
+ENGINES = {"m4rm": 0, "tc-i8": 1, "tc-f8": 2, "tc-f4": 3}
 
 
 def set_engine(name: str) -> None:
     """Select the product engine: "m4rm" (shared-memory Gray tables),
-    "tc-i8" or "tc-f8" (tcgen05 tensor cores). Results are identical."""
+    "tc-i8", "tc-f8" or "tc-f4" (tcgen05 tensor cores; tc-f4 is the
+    block-scaled kind::mxf4 MMA on e2m1 nibbles). Results are identical."""
     if name not in ENGINES:
         raise ValueError(f"engine {name!r} not in {sorted(ENGINES)}")
     check(load().gf2_set_engine(ENGINES[name]))

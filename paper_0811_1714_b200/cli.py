@@ -9,7 +9,7 @@
 Subcommands, flags, algorithm names, CSV columns and exit codes follow the
 reference CLI (cli.py:65-351): algorithms cubic, m4rm, m4rm-blocked,
 m4rm-t<t> (t = 1..8), strassen, auto; `check` exits 1 on a mismatch, file /
-dimension errors exit 2. Added: --engine (m4rm | tc-i8 | tc-f8) selects the
+dimension errors exit 2. Added: --engine (m4rm | tc-i8 | tc-f8 | tc-f4) selects the
 Strassen leaf engine. `check` cross-checks every variant against the
 device cubic product (the reference additionally uses its CPU oracle, which
 this package deliberately does not import).

@@ -15,7 +15,7 @@ int strassen_mul(const gf2_view &C, const gf2_view &A, const gf2_view &B, int64_
 void peel_split(int64_t m, int64_t l, int64_t n, int64_t cutoff, int64_t out[4]);
 
 std::atomic<int64_t> g_launches{0};
-int g_engine = 1;  // tcgen05 kind::i8: measured fastest base case
+int g_engine = 3;  // tcgen05 kind::mxf4: measured fastest base case
 static thread_local std::string t_err;
 
 int set_error(int code, const std::string &msg) {
@@ -99,7 +99,8 @@ int64_t gf2_launch_count(void) { return g_launches.load(); }
 int gf2_timer_enable(int on) { return timer_enable(on); }
 
 int gf2_set_engine(int engine) {
-    if (engine < 0 || engine > 2) return set_error(GF2_ERR_PARAMETER, "engine must be 0 (m4rm), 1 (tc-i8), 2 (tc-f8)");
+    if (engine < 0 || engine > 3)
+        return set_error(GF2_ERR_PARAMETER, "engine must be 0 (m4rm), 1 (tc-i8), 2 (tc-f8), 3 (tc-f4)");
     g_engine = engine;
     return GF2_OK;
 }

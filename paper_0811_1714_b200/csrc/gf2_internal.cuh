@@ -104,7 +104,7 @@ struct UmmaJob {
     unsigned maskA[7], maskB[7], maskC[7];
 };
 int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s);
-// multiply engine for every product (gf2_set_engine): 0 M4RM, 1 tcgen05 i8, 2 tcgen05 f8
+// multiply engine for every product (gf2_set_engine): 0 M4RM, 1 tcgen05 i8, 2 tcgen05 f8, 3 tcgen05 mxf4
 extern int g_engine;
 // Products below ~2^34 bit-ops run faster on the M4RM kernel than through
 // byte expansion + tensor cores (fixed costs dominate; tools/bench_configs.py:
@@ -114,7 +114,7 @@ constexpr double kTensorMinWork = 17179869184.0;  // 2^34
 inline int launch_product(const M4rmBatch &b, cudaStream_t s) {
     const double work = (double)b.m * (double)b.l * (double)b.n * (double)b.nprob;
     if (g_engine == 0 || work < kTensorMinWork) return launch_m4rm(b, s);
-    return launch_umma(b, g_engine == 1 ? 0 : 1, s);
+    return launch_umma(b, g_engine - 1, s);
 }
 int timer_enable(int on);
 int timer_begin(cudaStream_t s, double bitops);  // -1 when the timer is off

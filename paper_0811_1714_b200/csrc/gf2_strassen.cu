@@ -145,7 +145,7 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
             jb.maskB[i] = kSB[i];
             jb.maskC[i] = kSCT[i];
         }
-        if (rc == GF2_OK) rc = launch_umma_job(jb, g_engine == 1 ? 0 : 1, s);
+        if (rc == GF2_OK) rc = launch_umma_job(jb, g_engine - 1, s);
     }
     for (int lv = last - 1; lv >= 0 && rc == GF2_OK; --lv) {
         CombineArgs c{};
@@ -317,7 +317,7 @@ int m4rm_mul(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accumu
 int engine_mul(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accumulate, cudaStream_t s) {
     M4rmBatch mb{a.data, a.pitch, 0, b.data, b.pitch, 0, c.data, c.pitch, 0, a.nrows, a.ncols, b.ncols, 1, accumulate};
     if (g_engine == 0) return launch_m4rm(mb, s);
-    return launch_umma(mb, g_engine == 1 ? 0 : 1, s);  // explicit engine: no size heuristic
+    return launch_umma(mb, g_engine - 1, s);  // explicit engine: no size heuristic
 }
 
 // strassen.py:257-282 dispatch (+ peel_fixup strassen.py:219-249).

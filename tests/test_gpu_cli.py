@@ -49,6 +49,7 @@ def test_bench_csv_and_errors(tmp_path, capsys):
     assert all(float(r["min_s"]) <= float(r["mean_s"]) for r in rows)
     assert run("mul", str(tmp_path / "missing"), str(out), str(out)) == 2
     assert run("check", "--dims", "2x2x2", "--algo", "nope") == 2
+    prev = g.get_engine()
     assert run("params", "--engine", "tc-f8") == 0
     assert "engine=tc-f8" in capsys.readouterr().out
-    g.set_engine("tc-i8")
+    g.set_engine(prev)

@@ -1,4 +1,4 @@
-"""Parity of the tcgen05 tensor-core engines (kind::i8, kind::f8f6f4) with
+"""Parity of the tcgen05 tensor-core engines (kind::i8, kind::f8f6f4, kind::mxf4) with
 the oracle: the same product as M4RM, bit-exact including trailing bits."""
 
 import numpy as np
@@ -10,7 +10,7 @@ from oracle import gf2_port as P
 pytestmark = pytest.mark.gpu
 g = pytest.importorskip("paper_0811_1714_b200")
 
-ENGINES = ["m4rm", "tc-i8", "tc-f8"]
+ENGINES = ["m4rm", "tc-i8", "tc-f8", "tc-f4"]
 
 
 @pytest.fixture(autouse=True)
@@ -18,8 +18,9 @@ def _engine_reset():
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
+    prev = g.get_engine()
     yield
-    g.set_engine("m4rm")
+    g.set_engine(prev)
 
 
 def words(m):

@@ -38,9 +38,10 @@ def nccl_group():
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("engine", ["tc-i8", "m4rm"])
+@pytest.mark.parametrize("engine", ["tc-f4", "tc-i8", "m4rm"])
 def test_sharded_shards_match_full_product(nccl_group, engine):
     from paper_0811_1714_b200.sharded import mul_sharded, shard_rows
+    prev = g.get_engine()
     g.set_engine(engine)
     try:
         m, l, n, world = 3000, 2500, 1800, 4
@@ -53,7 +54,7 @@ def test_sharded_shards_match_full_product(nccl_group, engine):
             c_p = mul_sharded(a_p, b, g.MulParams(cutoff=512), npanels=3)
             assert np.array_equal(c_p.to_numpy(), full[r0:r1]), rank
     finally:
-        g.set_engine("tc-i8")
+        g.set_engine(prev)
 
 
 def test_sharded_cfg3_digest(nccl_group, digests):
