@@ -991,6 +991,14 @@ __global__ void __launch_bounds__(256) k_expand4_cols(ExpandArgs a) {
     }
 }
 
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\n@P mov.s32 %0, 1;\n}\n"
+        : "+r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ void umma_f4(uint32_t taddr, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc,
                                         uint32_t sfa, uint32_t sfb) {
     asm volatile(
@@ -1132,11 +1140,14 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
                 }
             }
         }
-    } else if (warp == 1 && lane == 0 && rank == 0) {
+    } else if (warp == 1 && rank == 0) {
+        // The whole warp walks the pipeline (warp-uniform control flow, so the
+        // descriptors stay in uniform registers); one elected lane issues.
         // block-scaled idesc: a/b format E2M1 (1) at bits 7/10, K-major both,
         // N >> 3 at 17, scale format UE8M0 at 23, M >> 4 at 24, scale ids 0
         const uint32_t idesc0 = (1u << 7) | (1u << 10) | (1u << 23) | ((uint32_t)(256 >> 4) << 24);
         const uint32_t sfa = tmem_base + F4_SF_COL, sfb = tmem_base + F4_SF_COL + 32;
+        const uint64_t adesc0 = smem_desc(sA, 16, 1024), bdesc0 = smem_desc(sB, 16, 1024);
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
@@ -1154,19 +1165,22 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
             for (int kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(bar_full + 8 * stage, phase);
                 tc_fence_after();
+                if (elect_one()) {
+                    const uint64_t ad = adesc0 + (uint64_t)((stage * F4_A_ST) >> 4);
+                    const uint64_t bd = bdesc0 + (uint64_t)((stage * F4_B_ST) >> 4);
 #pragma unroll
-                for (int k = 0; k < BK / 32; ++k) {
-                    const uint64_t ad = smem_desc(sA + stage * F4_A_ST + k * 32, 16, 1024);
-                    const uint64_t bd = smem_desc(sB + stage * F4_B_ST + k * 32, 16, 1024);
-                    umma_f4(taddr, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u, sfa, sfb);
+                    for (int k = 0; k < BK / 32; ++k)
+                        umma_f4(taddr, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u, sfa, sfb);
+                    umma_commit_cg<2>(bar_empty + 8 * stage);
                 }
-                umma_commit_cg<2>(bar_empty + 8 * stage);
+                __syncwarp();
                 if (++stage == F4_STG) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
-            umma_commit_cg<2>(bar_tfull + 8 * acc);
+            if (elect_one()) umma_commit_cg<2>(bar_tfull + 8 * acc);
+            __syncwarp();
         }
     } else if (warp >= 4) {
         const int q = warp & 3;
