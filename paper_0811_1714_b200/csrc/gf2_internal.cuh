@@ -23,6 +23,23 @@ __host__ __device__ inline u64 tail_mask(int64_t ncols) {
     return rem == 0 ? ~0ULL : (~0ULL << (kWordBits - rem));
 }
 
+// 32 x 32 bit transpose across a warp: lane L bit P <-> lane P bit L
+// (5 butterfly stages; at stage s the lanes swap the bits whose lane and
+// position s-bits differ).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+    const uint32_t masks[5] = {0xFFFF0000u, 0xFF00FF00u, 0xF0F0F0F0u, 0xCCCCCCCCu, 0xAAAAAAAAu};
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const int sh = 16 >> i;
+        const uint32_t m = masks[i];
+        const bool up = lane & sh;
+        const uint32_t give = up ? (x & ~m) : (x & m);
+        const uint32_t got = __shfl_xor_sync(0xffffffffu, give, sh);
+        x = up ? ((x & m) | (got >> sh)) : ((x & ~m) | (got << sh));
+    }
+    return x;
+}
+
 // Status plumbing ------------------------------------------------------
 int set_error(int code, const std::string &msg);
 int check_cuda(cudaError_t e, const char *what);
@@ -68,6 +85,7 @@ struct CombineArgs {
     int accumulate;
 };
 int launch_combine(const CombineArgs &a, cudaStream_t s);
+int launch_combine_t(const CombineArgs &a, cudaStream_t s);  // 7 transposed pre-add outputs
 int pool_setup();
 int launch_transpose(const gf2_view &out, const gf2_view &in, cudaStream_t s);
 int launch_cubic(const gf2_view &c, const gf2_view &a, const gf2_view &bt, int accumulate, cudaStream_t s);
@@ -102,6 +120,7 @@ struct UmmaJob {
     int fuse_pre;     // Strassen levels fused into the expansion: 0, 1 or 2
     int fuse_post, accumulate;
     unsigned maskA[7], maskB[7], maskC[7];
+    int b_trans;      // B given transposed (rows n, cols l, pitch pb); kind 2 only
 };
 int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s);
 // multiply engine for every product (gf2_set_engine): 0 M4RM, 1 tcgen05 i8, 2 tcgen05 f8, 3 tcgen05 mxf4

@@ -185,6 +185,70 @@ __global__ void k_combine_all(CombineArgs p, int64_t wblocks) {
     }
 }
 
+// Level-0 B pre-addition fused with the transpose the FP4 engine needs:
+// dst_q = (XOR_{i in mask[q]} quadrant_i(src))^T, q < 7. A block stages the
+// 4 quadrants' tiles (256 rows x 8 words each) in shared memory; warp w
+// transposes word column w of every quadrant (transpose32, linear, so the
+// XOR commutes with it) and writes each transposed row's 4 words with two
+// 16-byte stores.
+constexpr int CT_ROWS = 256, CT_WORDS = 8;
+constexpr int CT_SMEM = 4 * CT_ROWS * (CT_WORDS + 1) * 8;
+__global__ void __launch_bounds__(256) k_combine_t(CombineArgs p) {
+    extern __shared__ __align__(16) unsigned char ct_smem[];
+    u64(*tile)[CT_ROWS][CT_WORDS + 1] = reinterpret_cast<u64(*)[CT_ROWS][CT_WORDS + 1]>(ct_smem);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t w0 = (int64_t)blockIdx.x * CT_WORDS, r0 = (int64_t)blockIdx.y * CT_ROWS;
+    const u64 *sb = p.src + (int64_t)blockIdx.z * p.src_stride;
+    for (int i = 0; i < 4 * CT_ROWS * CT_WORDS / 256; ++i) {
+        const int idx = threadIdx.x + 256 * i;
+        const int qd = idx / (CT_ROWS * CT_WORDS), rem = idx % (CT_ROWS * CT_WORDS);
+        const int rr = rem / CT_WORDS, ww = rem % CT_WORDS;
+        const int64_t r = r0 + rr, w = w0 + ww;
+        tile[qd][rr][ww] = (r < p.R && w < p.W) ? __ldg(sb + p.src_off[qd] + r * p.src_pitch + w) : 0;
+    }
+    __syncthreads();
+    const int64_t w = w0 + warp;
+    if (w >= p.W) return;
+    const int ngroups = (int)min((int64_t)(CT_ROWS / 64), (p.R - r0 + 63) / 64);
+    const bool vec = ngroups == 4 && (p.dst_pitch % 2 == 0) && (p.dst_stride % 2 == 0);
+    u64 *db = p.dst + (int64_t)blockIdx.z * 7 * p.dst_stride;
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+        u64 T[4][4];  // [quadrant][64-row group]: transposed word of row 64w + 32 half + lane
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd)
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                const u64 x0 = tile[qd][64 * g + lane][warp], x1 = tile[qd][64 * g + 32 + lane][warp];
+                const uint32_t p0 = half ? (uint32_t)x0 : (uint32_t)(x0 >> 32);
+                const uint32_t p1 = half ? (uint32_t)x1 : (uint32_t)(x1 >> 32);
+                const uint32_t a = transpose32(__brev(p0), lane), b = transpose32(__brev(p1), lane);
+                T[qd][g] = __brevll(((u64)b << 32) | a);
+            }
+        const int64_t orow = w * 64 + half * 32 + lane;  // output row (< 64 W, always in range)
+#pragma unroll
+        for (int q = 0; q < 7; ++q) {
+            u64 o[4];
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                o[g] = 0;
+#pragma unroll
+                for (int qd = 0; qd < 4; ++qd)
+                    if (p.mask[q] & (1u << qd)) o[g] ^= T[qd][g];
+            }
+            u64 *drow = db + q * p.dst_stride + orow * p.dst_pitch + r0 / 64;
+            if (vec) {
+                reinterpret_cast<ulonglong2 *>(drow)[0] = make_ulonglong2(o[0], o[1]);
+                reinterpret_cast<ulonglong2 *>(drow)[1] = make_ulonglong2(o[2], o[3]);
+            } else {
+#pragma unroll
+                for (int g = 0; g < 4; ++g)
+                    if (g < ngroups) drow[g] = o[g];
+            }
+        }
+    }
+}
+
 inline dim3 row_grid(int64_t width, int64_t nrows, dim3 blk) {
     int64_t gx = (width + blk.x - 1) / blk.x;
     int64_t gy = (nrows + blk.y - 1) / blk.y;
@@ -277,4 +341,25 @@ int launch_combine(const CombineArgs &a, cudaStream_t s) {
     return check_cuda(cudaGetLastError(), "k_combine launch");
 }
 
+}  // namespace gf2
+
+namespace gf2 {
+// CombineArgs as for launch_combine with nq = 7 and 4 source quadrants of
+// R rows x W words; dst problems are 64 W rows x R / 64 words (pitch
+// dst_pitch, stride dst_stride, the 7 outputs of source problem p at
+// dst + (7p + q) dst_stride). R must be a multiple of 64.
+int launch_combine_t(const CombineArgs &a, cudaStream_t s) {
+    if (!a.R || !a.W || !a.nprob) return GF2_OK;
+    if (a.R % 64) return set_error(GF2_ERR_PARAMETER, "combine_t: rows not a multiple of 64");
+    static bool attr = false;
+    if (!attr) {
+        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_combine_t, cudaFuncAttributeMaxDynamicSharedMemorySize, CT_SMEM),
+                           "combine_t smem attr"));
+        attr = true;
+    }
+    dim3 grd((unsigned)((a.W + CT_WORDS - 1) / CT_WORDS), (unsigned)((a.R + CT_ROWS - 1) / CT_ROWS), (unsigned)a.nprob);
+    k_combine_t<<<grd, 256, CT_SMEM, s>>>(a);
+    note_launch();
+    return check_cuda(cudaGetLastError(), "k_combine_t launch");
+}
 }  // namespace gf2

@@ -44,6 +44,9 @@ int m4rm_view(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accum
     return launch_product(mb, s);
 }
 
+// the same quadrant mask on a transposed operand (X12 <-> X21)
+constexpr unsigned swap12(unsigned m) { return (m & 9u) | ((m & 2u) << 1) | ((m & 4u) >> 1); }
+
 // product q = 7p + i lands in these quadrants of C_p (transpose of kSC)
 constexpr unsigned kSCT[7] = {0xF, 0x1, 0x2, 0x4, 0xA, 0xE, 0xC};
 
@@ -67,6 +70,9 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
     static const int fuse_env = getenv("GF2_FUSE_LEVELS") ? atoi(getenv("GF2_FUSE_LEVELS")) : 1;
     const int fp = (depth >= 2 && fuse_env >= 2) ? 2 : 1;
     const int lastA = depth - fp;             // deepest materialized A/B level
+    // FP4 engine: its MMA wants B K-major, so B0 is transposed once here and
+    // the B side of the recursion runs on B^T (quadrants 12 and 21 swap)
+    const bool bt = g_engine == 3;
     int64_t offA[24], offB[24], offC[24], total = 0;
     for (int i = 1; i <= last; ++i) {
         if (i <= lastA) {
@@ -78,6 +84,10 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
         offC[i] = total;
         total += P[i] * M[i] * Nw[i];
     }
+    // B^T of the whole operand is materialized only when no pre-addition level
+    // is (lastA == 0); otherwise level 0's B pre-addition writes transposed
+    const int64_t offBt0 = total;
+    if (bt && lastA == 0) total += N[0] * Lw[0];
     GF2_TRY(pool_setup());
     u64 *ws = nullptr;
     if (total) {
@@ -88,19 +98,38 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
         }
     }
     int rc = GF2_OK;
+    gf2_view Bt0{ws + offBt0, Lw[0], N[0], L[0]};
+    if (bt && lastA == 0) rc = launch_transpose(Bt0, B0, s);
     for (int lv = 0; lv < lastA && rc == GF2_OK; ++lv) {
         for (int side = 0; side < 2 && rc == GF2_OK; ++side) {
             CombineArgs c{};
             const bool isA = side == 0;
-            const int64_t R = isA ? M[lv + 1] : L[lv + 1];
-            const int64_t W = isA ? Lw[lv + 1] : Nw[lv + 1];
+            if (bt && !isA && lv == 0) {  // (quadrant combinations of B0)^T
+                c.src = B0.data;
+                c.src_pitch = B0.pitch;
+                c.R = L[1];
+                c.W = Nw[1];
+                c.src_off[1] = c.W;
+                c.src_off[2] = c.R * c.src_pitch;
+                c.src_off[3] = c.src_off[2] + c.W;
+                c.dst = ws + offB[1];
+                c.dst_pitch = Lw[1];
+                c.dst_stride = N[1] * Lw[1];
+                for (int q = 0; q < 7; ++q) c.mask[q] = kSB[q];
+                c.nq = 7;
+                c.nprob = 1;
+                rc = launch_combine_t(c, s);
+                continue;
+            }
+            const int64_t R = isA ? M[lv + 1] : (bt ? N[lv + 1] : L[lv + 1]);
+            const int64_t W = isA ? Lw[lv + 1] : (bt ? Lw[lv + 1] : Nw[lv + 1]);
             if (lv == 0) {
-                c.src = isA ? A0.data : B0.data;
-                c.src_pitch = isA ? A0.pitch : B0.pitch;
+                c.src = isA ? A0.data : (bt ? Bt0.data : B0.data);
+                c.src_pitch = isA ? A0.pitch : (bt ? Bt0.pitch : B0.pitch);
             } else {
                 c.src = ws + (isA ? offA[lv] : offB[lv]);
-                c.src_pitch = isA ? Lw[lv] : Nw[lv];
-                c.src_stride = (isA ? M[lv] : L[lv]) * c.src_pitch;
+                c.src_pitch = isA ? Lw[lv] : (bt ? Lw[lv] : Nw[lv]);
+                c.src_stride = (isA ? M[lv] : (bt ? N[lv] : L[lv])) * c.src_pitch;
             }
             c.src_off[1] = W;
             c.src_off[2] = R * c.src_pitch;
@@ -110,7 +139,7 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
             c.dst_stride = 7 * R * W;
             for (int q = 0; q < 7; ++q) {
                 c.dst_off[q] = q * R * W;
-                c.mask[q] = isA ? kSA[q] : kSB[q];
+                c.mask[q] = isA ? kSA[q] : (bt ? swap12(kSB[q]) : kSB[q]);
             }
             c.nq = 7;
             c.R = R;
@@ -123,11 +152,14 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
         UmmaJob jb{};
         if (lastA == 0) {
             jb.A = A0.data; jb.pa = A0.pitch;
-            jb.B = B0.data; jb.pb = B0.pitch;
+            jb.B = bt ? Bt0.data : B0.data; jb.pb = bt ? Bt0.pitch : B0.pitch;
         } else {
             jb.A = ws + offA[lastA]; jb.pa = Lw[lastA]; jb.sa = M[lastA] * Lw[lastA];
-            jb.B = ws + offB[lastA]; jb.pb = Nw[lastA]; jb.sb = L[lastA] * Nw[lastA];
+            jb.B = ws + offB[lastA];
+            jb.pb = bt ? Lw[lastA] : Nw[lastA];
+            jb.sb = bt ? N[lastA] * Lw[lastA] : L[lastA] * Nw[lastA];
         }
+        jb.b_trans = bt ? 1 : 0;
         if (last == 0) {
             jb.C = C0.data; jb.pc = C0.pitch;
             if (!accumulate) rc = launch_ewise(C0, nullptr, nullptr, 0, s);
@@ -142,7 +174,7 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
         jb.fuse_post = 1;
         for (int i = 0; i < 7; ++i) {
             jb.maskA[i] = kSA[i];
-            jb.maskB[i] = kSB[i];
+            jb.maskB[i] = bt ? swap12(kSB[i]) : kSB[i];
             jb.maskC[i] = kSCT[i];
         }
         if (rc == GF2_OK) rc = launch_umma_job(jb, g_engine - 1, s);

@@ -1,8 +1,7 @@
 // Structural kernels around the multiply path:
-//   k_transpose  -- bit-matrix transpose (core.py:374-376), 64x64 blocks per
-//                   warp with __ballot_sync: lane r holds rows r and r+32 of
-//                   the block; one ballot per (column, half) yields 32 bits of
-//                   a transposed row.
+//   k_transpose  -- bit-matrix transpose (core.py:374-376): shared-memory
+//                   staged 256-row tiles, 64 x 64 blocks per warp as four
+//                   warp-wide 32 x 32 butterfly transposes.
 //   k_cubic      -- mul_cubic (cubic.py:76-102): C[i, j] = parity(A_i & (B^T)_j)
 //                   over words, for narrow B (the reference's n < 64 path).
 //   k_copy_cols  -- dst[:, c0 : c0+n) = src[:, 0 : n) for ANY bit offset c0
@@ -14,34 +13,43 @@ namespace gf2 {
 
 namespace {
 
-// One warp per 64x64 block: out[c][r] = in[r][c].
-__global__ void k_transpose(const u64 *__restrict__ in, int64_t pin, u64 *__restrict__ out, int64_t pout,
-                            int64_t rows, int64_t cols) {
-    const int lane = threadIdx.x & 31;
-    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t wcols = words_per_row(cols), wrows = words_per_row(rows);
-    const int64_t nblocks = wrows * wcols;
-    if (wid >= nblocks) return;
-    const int64_t br = wid / wcols, bc = wid % wcols;  // block row (input rows/64), block col (input words)
-    const int64_t r0 = br * 64;
-    const u64 tm = (bc == wcols - 1) ? tail_mask(cols) : ~0ULL;
-    const u64 lo = (r0 + lane < rows) ? (in[(r0 + lane) * pin + bc] & tm) : 0;
-    const u64 hi = (r0 + 32 + lane < rows) ? (in[(r0 + 32 + lane) * pin + bc] & tm) : 0;
-    // transposed row c (= input column bc*64 + c) has input rows r0..r0+63
-    // at bits 63..0: rows r0..r0+31 -> high half, r0+32..r0+63 -> low half
-    u64 w0 = 0, w1 = 0;  // lane keeps transposed rows `lane` and `lane + 32`
-#pragma unroll 8
-    for (int c = 0; c < 64; ++c) {
-        const unsigned blo = __ballot_sync(0xffffffffu, (lo >> (63 - c)) & 1);
-        const unsigned bhi = __ballot_sync(0xffffffffu, (hi >> (63 - c)) & 1);
-        const u64 w = ((u64)__brev(blo) << 32) | (u64)__brev(bhi);
-        if (c == lane) w0 = w;
-        if (c == lane + 32) w1 = w;
+// out[c][r] = in[r][c]. A block stages 256 input rows x 8 words in shared
+// memory (coalesced row segments); warp w then transposes word column w in
+// 64-row groups with four warp-wide 32 x 32 butterflies each (transpose32).
+constexpr int TR_ROWS = 256, TR_WORDS = 8;
+__global__ void __launch_bounds__(256) k_transpose(const u64 *__restrict__ in, int64_t pin, u64 *__restrict__ out,
+                                                   int64_t pout, int64_t rows, int64_t cols) {
+    __shared__ u64 tile[TR_ROWS][TR_WORDS + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t wcols = words_per_row(cols);
+    const int64_t w0 = (int64_t)blockIdx.x * TR_WORDS, r0 = (int64_t)blockIdx.y * TR_ROWS;
+#pragma unroll
+    for (int i = 0; i < TR_ROWS * TR_WORDS / 256; ++i) {
+        const int idx = threadIdx.x + 256 * i;
+        const int rr = idx / TR_WORDS, ww = idx % TR_WORDS;
+        const int64_t r = r0 + rr, w = w0 + ww;
+        u64 x = 0;
+        if (r < rows && w < wcols) x = in[r * pin + w] & (w == wcols - 1 ? tail_mask(cols) : ~0ULL);
+        tile[rr][ww] = x;
     }
+    __syncthreads();
+    const int64_t w = w0 + warp;
+    if (w >= wcols) return;
     // bits of input rows beyond `rows` are zero, so output tails stay clean
-    const int64_t oc = bc * 64 + lane;
-    if (oc < cols) out[oc * pout + br] = w0;
-    if (oc + 32 < cols) out[(oc + 32) * pout + br] = w1;
+    const int64_t oc = w * 64 + lane;
+#pragma unroll
+    for (int g = 0; g < TR_ROWS / 64; ++g) {
+        if (r0 + 64 * g >= rows) break;
+        const u64 x0 = tile[64 * g + lane][warp], x1 = tile[64 * g + 32 + lane][warp];
+        // lane c: bit i of cXa / cXb = input row i / 32 + i of column c (or c + 32)
+        const uint32_t c0a = transpose32(__brev((uint32_t)(x0 >> 32)), lane);
+        const uint32_t c0b = transpose32(__brev((uint32_t)(x1 >> 32)), lane);
+        const uint32_t c1a = transpose32(__brev((uint32_t)x0), lane);
+        const uint32_t c1b = transpose32(__brev((uint32_t)x1), lane);
+        const int64_t ow = r0 / 64 + g;  // output word (MSB-first: row i at bit 63 - i)
+        if (oc < cols) out[oc * pout + ow] = __brevll(((u64)c0b << 32) | c0a);
+        if (oc + 32 < cols) out[(oc + 32) * pout + ow] = __brevll(((u64)c1b << 32) | c1a);
+    }
 }
 
 // Narrow-B cubic product: one thread per (row i, output word); BT is B^T.
@@ -104,11 +112,10 @@ __global__ void k_copy_cols(const u64 *__restrict__ src, int64_t ps, u64 *__rest
 }  // namespace
 
 int launch_transpose(const gf2_view &out, const gf2_view &in, cudaStream_t s) {
-    const int64_t blocks = words_per_row(in.nrows) * words_per_row(in.ncols);
-    if (!blocks) return GF2_OK;
-    const int64_t threads = blocks * 32;
-    k_transpose<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(in.data, in.pitch, out.data, out.pitch, in.nrows,
-                                                                   in.ncols);
+    const int64_t wcols = words_per_row(in.ncols);
+    if (!wcols || !in.nrows) return GF2_OK;
+    dim3 grd((unsigned)((wcols + TR_WORDS - 1) / TR_WORDS), (unsigned)((in.nrows + TR_ROWS - 1) / TR_ROWS));
+    k_transpose<<<grd, 256, 0, s>>>(in.data, in.pitch, out.data, out.pitch, in.nrows, in.ncols);
     note_launch();
     return check_cuda(cudaGetLastError(), "k_transpose launch");
 }

@@ -98,6 +98,14 @@ __device__ __forceinline__ void umma(uint32_t taddr, uint64_t ad, uint64_t bd, u
             "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(taddr),
             "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
 }
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\n@P mov.s32 %0, 1;\n}\n"
+        : "+r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
                  : "memory");
@@ -418,10 +426,12 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
                 }
             }
         }
-    } else if (warp == 1 && lane == 0 && rank == 0) {
-        // ---------------- MMA issuer (leader CTA)
+    } else if (warp == 1 && rank == 0) {
+        // ---------------- MMA issuer (leader CTA): warp-uniform loop, one
+        // elected lane issues (descriptors stay in uniform registers)
         const uint32_t idesc = (KIND == 0 ? (2u << 4) : (1u << 4)) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) |
                                ((uint32_t)(G::MT >> 4) << 24);
+        const uint64_t adesc0 = smem_desc(sA, 16, 1024), bdesc0 = smem_desc(sB, CG == 1 ? G::B_ST / 2 : 16, 1024);
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
@@ -437,19 +447,22 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
             for (int kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(bar_full + 8 * stage, phase);
                 tc_fence_after();
+                if (elect_one()) {
+                    const uint64_t ad = adesc0 + (uint64_t)((stage * G::A_ST) >> 4);
+                    const uint64_t bd = bdesc0 + (uint64_t)((stage * G::B_ST) >> 4);
 #pragma unroll
-                for (int k = 0; k < BK / 32; ++k) {
-                    const uint64_t ad = smem_desc(sA + stage * G::A_ST + k * 32, 16, 1024);
-                    const uint64_t bd = smem_desc(sB + stage * G::B_ST + k * 32 * 128, CG == 1 ? G::B_ST / 2 : 16, 1024);
-                    umma_cg<KIND, CG>(taddr, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                    for (int k = 0; k < BK / 32; ++k)  // A: +32 B along K; B (MN-major): +32 rows of 128 B
+                        umma_cg<KIND, CG>(taddr, ad + 2 * k, bd + 256 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                    umma_commit_cg<CG>(bar_empty + 8 * stage);
                 }
-                umma_commit_cg<CG>(bar_empty + 8 * stage);
+                __syncwarp();
                 if (++stage == G::STG) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
-            umma_commit_cg<CG>(bar_tfull + 8 * acc);
+            if (elect_one()) umma_commit_cg<CG>(bar_tfull + 8 * acc);
+            __syncwarp();
         }
     } else if (warp >= 4) {
         // ---------------- epilogue: TMEM -> parity bits -> C (each CTA its rows)
@@ -895,23 +908,6 @@ __global__ void __launch_bounds__(256) k_expand4_rows(ExpandArgs a) {
     }
 }
 
-// 32 x 32 bit transpose across a warp: lane L bit P <-> lane P bit L
-// (5 butterfly stages; at stage s the lanes swap the bits whose lane and
-// position s-bits differ).
-__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
-    const uint32_t masks[5] = {0xFFFF0000u, 0xFF00FF00u, 0xF0F0F0F0u, 0xCCCCCCCCu, 0xAAAAAAAAu};
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-        const int sh = 16 >> i;
-        const uint32_t m = masks[i];
-        const bool up = lane & sh;
-        const uint32_t give = up ? (x & ~m) : (x & m);
-        const uint32_t got = __shfl_xor_sync(0xffffffffu, give, sh);
-        x = up ? ((x & m) | (got >> sh)) : ((x & ~m) | (got << sh));
-    }
-    return x;
-}
-
 // B side, transposed. A block stages 256 K rows x 16 words (coalesced 128 B
 // row segments, fused quadrant XORs) in shared memory; each warp then owns
 // 2 words: per 64-row K block, four warp-wide 32 x 32 transposes turn the
@@ -991,14 +987,6 @@ __global__ void __launch_bounds__(256) k_expand4_cols(ExpandArgs a) {
     }
 }
 
-__device__ __forceinline__ bool elect_one() {
-    uint32_t pred = 0;
-    asm volatile(
-        "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\n@P mov.s32 %0, 1;\n}\n"
-        : "+r"(pred));
-    return pred != 0;
-}
-
 __device__ __forceinline__ void umma_f4(uint32_t taddr, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc,
                                         uint32_t sfa, uint32_t sfb) {
     asm volatile(
@@ -1049,9 +1037,8 @@ __device__ __forceinline__ void store_row_f4(const UArgs &p, const uint32_t *pac
     }
 }
 
-// Persistent CTA-pair kernel (cluster of 2, tcgen05.mma.cta_group::2), tile
-// 256 x 224 (the last column tile of a row may be narrower), 128 B = 256 K
-// entries per stage. TMEM: accumulators at columns 0 and 224, scale factors
+// Persistent CTA-pair kernel (cluster of 2, tcgen05.mma.cta_group::2), tiles
+// 256 x (32..224), 128 B = 256 K entries per stage. TMEM: accumulators at columns 0 and 224, scale factors
 // (all 0x7F) at 448..511 in both CTAs.
 __global__ void __launch_bounds__(UMMA_THREADS, 1)
     k_umma_f4(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, UArgs p) {
@@ -1109,11 +1096,13 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
 
     const int64_t tiles_per_chunk = p.nprob * p.mt * p.nt;
     const int64_t ntiles = tiles_per_chunk * p.nchunks;
-    auto tile_width = [&](int ntile) -> int {
-        const int64_t left = p.n - (int64_t)ntile * F4_BN;
-        const int w = (int)(left < F4_BN ? left : F4_BN);
-        return (w + 15) & ~15;
-    };
+    // column tiles: the row's 32-column groups spread evenly over p.nt tiles
+    // of <= 7 groups (4096 columns: 14 x 224 + 5 x 192), so no tile is a
+    // narrow, TMA-bound remainder; starts stay 32-bit-word aligned
+    const int ngroups = (int)((p.n + 31) / 32);
+    const int gq = ngroups / p.nt, gr = ngroups % p.nt;
+    auto tile_g0 = [&](int ntile) -> int { return ntile * gq + min(ntile, gr); };
+    auto tile_width = [&](int ntile) -> int { return 32 * (gq + (ntile < gr ? 1 : 0)); };
 
     if (warp == 0 && lane == 0) {
         int stage = 0;
@@ -1127,7 +1116,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
             const int kb0 = chunk * p.kchunk_blocks;
             const int kb1 = min(kb0 + p.kchunk_blocks, p.kblocks);
             const int arow = mtile * 256 + (int)rank * BM;
-            const int brow = ntile * F4_BN + (int)rank * (tile_width(ntile) / 2);
+            const int brow = 32 * tile_g0(ntile) + (int)rank * (tile_width(ntile) / 2);
             for (int kb = kb0; kb < kb1; ++kb) {
                 const uint32_t fb = bar_full + 8 * stage;
                 mbar_wait(bar_empty + 8 * stage, phase ^ 1);
@@ -1190,7 +1179,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
             const int prob = (int)(r / (p.mt * p.nt));
             r %= (p.mt * p.nt);
             const int mtile = (int)(r / p.nt), ntile = (int)(r % p.nt);
-            const int nch = (tile_width(ntile) + 31) >> 5;
+            const int nch = tile_width(ntile) >> 5;
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             mbar_wait(bar_tfull + 8 * acc, acc_phase);
@@ -1213,7 +1202,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
             tc_fence_before();
             mbar_arrive_leader(bar_tempty + 8 * acc);
             const int64_t row = (int64_t)mtile * 256 + (int64_t)rank * BM + q * 32 + lane;
-            store_row_f4(p, packed, row, (int64_t)ntile * (F4_BN / 32), nch, p.q0 + prob);
+            store_row_f4(p, packed, row, (int64_t)tile_g0(ntile), nch, p.q0 + prob);
         }
     }
     tc_fence_before();
@@ -1342,12 +1331,16 @@ int launch_umma_f4(const UmmaJob &jb, int64_t nprob, cudaStream_t s) {
     ea.qoff2[1] = jb.l / 64; ea.qoff2[2] = jb.m * jb.pa; ea.qoff2[3] = ea.qoff2[1] + ea.qoff2[2];
     for (int i = 0; i < 7; ++i) ea.mask[i] = jb.maskA[i];
     ea.dst = a4; ea.dp = kb; ea.dstride = jb.m * kb; ea.rows = jb.m; ea.cols = jb.l;
+    // B side: row expansion of B^T when given transposed, else the
+    // transposing column expansion of B
+    const bool bt = jb.b_trans != 0;
+    const int64_t brows = bt ? jb.n : jb.l, bcols = bt ? jb.l : jb.n;
     ExpandArgs eb{};
     eb.src = jb.B; eb.sp = jb.pb; eb.sstride = jb.sb; eb.levels = jb.fuse_pre;
-    eb.qoff[1] = f2 * jb.n / 64; eb.qoff[2] = f2 * jb.l * jb.pb; eb.qoff[3] = eb.qoff[1] + eb.qoff[2];
-    eb.qoff2[1] = jb.n / 64; eb.qoff2[2] = jb.l * jb.pb; eb.qoff2[3] = eb.qoff2[1] + eb.qoff2[2];
+    eb.qoff[1] = f2 * bcols / 64; eb.qoff[2] = f2 * brows * jb.pb; eb.qoff[3] = eb.qoff[1] + eb.qoff[2];
+    eb.qoff2[1] = bcols / 64; eb.qoff2[2] = brows * jb.pb; eb.qoff2[3] = eb.qoff2[1] + eb.qoff2[2];
     for (int i = 0; i < 7; ++i) eb.mask[i] = jb.maskB[i];
-    eb.dst = b4; eb.dp = kb; eb.dstride = np * kb; eb.rows = jb.l; eb.cols = jb.n;
+    eb.dst = b4; eb.dp = kb; eb.dstride = np * kb; eb.rows = brows; eb.cols = bcols;
 
     UArgs ua{};
     ua.C = jb.C; ua.pc = jb.pc; ua.sc = jb.sc;
@@ -1378,10 +1371,11 @@ int launch_umma_f4(const UmmaJob &jb, int64_t nprob, cudaStream_t s) {
         ea.q0 = eb.q0 = ua.q0 = q0;
         ua.nprob = nq;
         rc = launch_expand4(ea, nq, false, s);
-        if (rc == GF2_OK) rc = launch_expand4(eb, nq, true, s);
+        if (rc == GF2_OK) rc = launch_expand4(eb, nq, !bt, s);
         CUtensorMap ta, tb;
         if (rc == GF2_OK) rc = make_map(&ta, a4, (uint64_t)kb, (uint64_t)jb.m, (uint64_t)nq, kb, jb.m * kb);
-        if (rc == GF2_OK) rc = make_map(&tb, b4, (uint64_t)kb, (uint64_t)np, (uint64_t)nq, kb, np * kb, F4_BNH);
+        if (rc == GF2_OK)  // rows past n (never written on the B^T path) read as zeros
+            rc = make_map(&tb, b4, (uint64_t)kb, (uint64_t)jb.n, (uint64_t)nq, kb, np * kb, F4_BNH);
         if (rc != GF2_OK) break;
         const int64_t ntiles = (int64_t)ua.nchunks * nq * ua.mt * ua.nt;
         const int64_t pairs = std::min<int64_t>(ntiles, g_sms / 2);
