@@ -1346,7 +1346,9 @@ int launch_umma_f4(const UmmaJob &jb, int64_t nprob, cudaStream_t s) {
     ua.C = jb.C; ua.pc = jb.pc; ua.sc = jb.sc;
     ua.m = jb.m; ua.n = jb.n; ua.Wn = words_per_row(jb.n);
     ua.mt = (int)((jb.m + 255) / 256);
-    ua.nt = (int)((jb.n + F4_BN - 1) / F4_BN);
+    // GF2_F4_BN: maximum column-tile width (tuning knob; 224 measured best)
+    static const int f4bn = getenv("GF2_F4_BN") ? std::max(32, std::min(F4_BN, atoi(getenv("GF2_F4_BN")))) : F4_BN;
+    ua.nt = (int)((jb.n + f4bn - 1) / f4bn);
     ua.kblocks = (int)((kb + BK - 1) / BK);
     ua.kchunk_blocks = (int)(F4_KCHUNK / (2 * BK));
     ua.nchunks = (ua.kblocks + ua.kchunk_blocks - 1) / ua.kchunk_blocks;

@@ -19,9 +19,11 @@ from .errors import DimensionError, ParameterError
 
 _WORD = 64
 
-# Crossover chosen for the B200: below it a single M4RM
-# launch fills the GPU better than a level of 7 sub-products plus 15 adds.
-GPU_CUTOFF = 4096
+# Crossover chosen for the B200 with the tc-f4 base case (DESIGN.md §4.3,
+# tools/bench_configs.py --cutoff): leaves of 8192 keep the FP4 GEMM at ~0.94
+# of its peak; another level (4096 leaves) costs more in additions and
+# expansion than its 1/8 fewer MACs save (cfg3 1.08 vs 1.15 ms, cfg5 57 vs 67).
+GPU_CUTOFF = 8192
 
 
 @dataclass

@@ -2,7 +2,8 @@
 reports the headline cfg3 line). Device-resident inputs, CUDA-event timing,
 warm-up excluded, L2 flushed between reps, every result digest-verified.
 
-    python tools/bench_configs.py [--reps R] [--engine tc-i8|tc-f8|m4rm]
+    python tools/bench_configs.py [--reps R] [--engine tc-f4|tc-i8|tc-f8|m4rm]
+                                  [--cutoff C]  (overrides the device default)
 """
 
 import argparse
@@ -41,10 +42,13 @@ def timed(fn, reps, flush):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=5)
-    ap.add_argument("--engine", default="tc-i8")
+    ap.add_argument("--engine", default="tc-f4")
+    ap.add_argument("--cutoff", type=int, default=0)
     ap.add_argument("--skip-cfg5", action="store_true")
     args = ap.parse_args()
     g.set_engine(args.engine)
+    if args.cutoff:
+        g.strassen.GPU_CUTOFF = args.cutoff
     torch.cuda.set_device(0)
     dig = json.load(open(os.path.join(ROOT, "tests", "golden", "digests.json")))
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
@@ -54,6 +58,7 @@ def main():
         out, tmin, tmean = timed(fn, args.reps, flush)
         m, l, n = mln
         d = {"cfg": cfg, "call": call, "m": m, "l": l, "n": n, "engine": args.engine,
+             "gpu_cutoff": g.strassen.GPU_CUTOFF,
              "ms_min": tmin, "ms_mean": tmean, "bitops_per_s": m * l * n / (tmin * 1e-3),
              "verified_sha256": digest(out() if callable(out) else out) == dig[key]}
         if extra:
@@ -104,7 +109,7 @@ def main():
             g.addmul(c, a, b)
             return c
         rec("cfg5", "C0 copy + addmul(C,A,B)", (n,) * 3, addmul5, "cfg5_addmul")
-    out = os.path.join(ROOT, "gpurun_out", f"configs_{args.engine}.jsonl")
+    out = os.path.join(ROOT, "gpurun_out", f"configs_{args.engine}_c{g.strassen.GPU_CUTOFF}.jsonl")
     os.makedirs(os.path.dirname(out), exist_ok=True)
     with open(out, "w") as fh:
         for r in rows:
