@@ -144,6 +144,10 @@ int gf2_upload(const gf2_view *dst, const uint64_t *host, int64_t host_stride, v
     const int64_t w = words_per_row(dst->ncols);
     if (!dst->nrows || !w) return GF2_OK;
     if (!host || host_stride < w) return set_error(GF2_ERR_PARAMETER, "bad host buffer / stride");
+    if (dst->pitch == w && host_stride == w)  // both dense: one linear DMA
+        return check_cuda(cudaMemcpyAsync(dst->data, host, (size_t)(w * dst->nrows) * 8, cudaMemcpyHostToDevice,
+                                          (cudaStream_t)stream),
+                          "upload");
     return check_cuda(cudaMemcpy2DAsync(dst->data, dst->pitch * 8, host, host_stride * 8, w * 8, dst->nrows,
                                         cudaMemcpyHostToDevice, (cudaStream_t)stream),
                       "upload");
@@ -154,6 +158,10 @@ int gf2_download(const gf2_view *src, uint64_t *host, int64_t host_stride, void 
     const int64_t w = words_per_row(src->ncols);
     if (!src->nrows || !w) return GF2_OK;
     if (!host || host_stride < w) return set_error(GF2_ERR_PARAMETER, "bad host buffer / stride");
+    if (src->pitch == w && host_stride == w)
+        return check_cuda(cudaMemcpyAsync(host, src->data, (size_t)(w * src->nrows) * 8, cudaMemcpyDeviceToHost,
+                                          (cudaStream_t)stream),
+                          "download");
     return check_cuda(cudaMemcpy2DAsync(host, host_stride * 8, src->data, src->pitch * 8, w * 8, src->nrows,
                                         cudaMemcpyDeviceToHost, (cudaStream_t)stream),
                       "download");

@@ -66,6 +66,7 @@ inline gf2_view sub_view(const gf2_view &v, int64_t r0, int64_t c0, int64_t nr, 
 int launch_random(const gf2_view &v, u64 seed, int64_t row_base, cudaStream_t s);
 int launch_bernoulli(const gf2_view &v, u64 seed, u64 thresh, int64_t row_base, cudaStream_t s);
 int launch_ewise(const gf2_view &out, const gf2_view *a, const gf2_view *b, int op, cudaStream_t s);
+int launch_zero(const gf2_view &v, cudaStream_t s);
 
 // Batched XOR-combine used by the breadth-first Strassen-Winograd:
 // for output o = p * nq + q (p < nprob, q < nq):

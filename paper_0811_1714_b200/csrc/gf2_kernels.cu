@@ -304,6 +304,16 @@ int launch_ewise(const gf2_view &out, const gf2_view *a, const gf2_view *b, int 
     return check_cuda(cudaGetLastError(), "k_ewise launch");
 }
 
+// Zero a view: a 2-D memset when it covers whole words, else the masked
+// k_ewise (bits beyond a ragged right edge belong to the parent matrix).
+int launch_zero(const gf2_view &v, cudaStream_t s) {
+    if (!v.nrows || !v.ncols) return GF2_OK;
+    if (v.ncols % kWordBits) return launch_ewise(v, nullptr, nullptr, 0, s);
+    return check_cuda(cudaMemset2DAsync(v.data, (size_t)v.pitch * 8, 0, (size_t)(v.ncols / kWordBits) * 8,
+                                        (size_t)v.nrows, s),
+                      "zero");
+}
+
 int launch_combine(const CombineArgs &a, cudaStream_t s) {
     if (!a.R || !a.W || !a.nprob) return GF2_OK;
     // 16-byte path when every address the kernel forms is 16-byte aligned

@@ -162,7 +162,7 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
         jb.b_trans = bt ? 1 : 0;
         if (last == 0) {
             jb.C = C0.data; jb.pc = C0.pitch;
-            if (!accumulate) rc = launch_ewise(C0, nullptr, nullptr, 0, s);
+            if (!accumulate) rc = launch_zero(C0, s);
         } else {
             jb.C = ws + offC[last]; jb.pc = Nw[last]; jb.sc = M[last] * Nw[last];
             rc = check_cuda(cudaMemsetAsync(ws + offC[last], 0, (size_t)(P[last] * M[last] * Nw[last]) * 8, s),

@@ -1,7 +1,7 @@
 // Structural kernels around the multiply path:
 //   k_transpose  -- bit-matrix transpose (core.py:374-376): shared-memory
-//                   staged 256-row tiles, 64 x 64 blocks per warp as four
-//                   warp-wide 32 x 32 butterfly transposes.
+//                   staged 512-row tiles, 64 x 64 blocks per warp as four
+//                   warp-wide 32 x 32 butterfly transposes, staged output.
 //   k_cubic      -- mul_cubic (cubic.py:76-102): C[i, j] = parity(A_i & (B^T)_j)
 //                   over words, for narrow B (the reference's n < 64 path).
 //   k_copy_cols  -- dst[:, c0 : c0+n) = src[:, 0 : n) for ANY bit offset c0
@@ -13,15 +13,18 @@ namespace gf2 {
 
 namespace {
 
-// out[c][r] = in[r][c]. A block stages 256 input rows x 8 words in shared
-// memory (coalesced row segments); warp w then transposes word column w in
-// 64-row groups with four warp-wide 32 x 32 butterflies each (transpose32).
-constexpr int TR_ROWS = 256, TR_WORDS = 8;
+// out[c][r] = in[r][c]. A block stages 512 input rows x 4 words (one 32-byte
+// sector per row) in shared memory; each warp transposes 64 x 64 blocks with
+// four warp-wide 32 x 32 butterflies (transpose32) into a shared output tile
+// (256 rows x 8 words), written back as 16-byte stores, 64 contiguous bytes
+// per output row.
+constexpr int TR_ROWS = 512, TR_WORDS = 4, TR_OUT_WORDS = TR_ROWS / 64;
 __global__ void __launch_bounds__(256) k_transpose(const u64 *__restrict__ in, int64_t pin, u64 *__restrict__ out,
                                                    int64_t pout, int64_t rows, int64_t cols) {
     __shared__ u64 tile[TR_ROWS][TR_WORDS + 1];
+    __shared__ u64 stg[64 * TR_WORDS][TR_OUT_WORDS + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t wcols = words_per_row(cols);
+    const int64_t wcols = words_per_row(cols), wrows = words_per_row(rows);
     const int64_t w0 = (int64_t)blockIdx.x * TR_WORDS, r0 = (int64_t)blockIdx.y * TR_ROWS;
 #pragma unroll
     for (int i = 0; i < TR_ROWS * TR_WORDS / 256; ++i) {
@@ -33,22 +36,34 @@ __global__ void __launch_bounds__(256) k_transpose(const u64 *__restrict__ in, i
         tile[rr][ww] = x;
     }
     __syncthreads();
-    const int64_t w = w0 + warp;
-    if (w >= wcols) return;
-    // bits of input rows beyond `rows` are zero, so output tails stay clean
-    const int64_t oc = w * 64 + lane;
-#pragma unroll
-    for (int g = 0; g < TR_ROWS / 64; ++g) {
-        if (r0 + 64 * g >= rows) break;
-        const u64 x0 = tile[64 * g + lane][warp], x1 = tile[64 * g + 32 + lane][warp];
-        // lane c: bit i of cXa / cXb = input row i / 32 + i of column c (or c + 32)
+    // units: (word column, 64-row group); bits of rows beyond `rows` are zero
+#pragma unroll 1
+    for (int u = warp; u < TR_WORDS * TR_OUT_WORDS; u += 8) {
+        const int ww = u % TR_WORDS, g = u / TR_WORDS;
+        const u64 x0 = tile[64 * g + lane][ww], x1 = tile[64 * g + 32 + lane][ww];
         const uint32_t c0a = transpose32(__brev((uint32_t)(x0 >> 32)), lane);
         const uint32_t c0b = transpose32(__brev((uint32_t)(x1 >> 32)), lane);
         const uint32_t c1a = transpose32(__brev((uint32_t)x0), lane);
         const uint32_t c1b = transpose32(__brev((uint32_t)x1), lane);
-        const int64_t ow = r0 / 64 + g;  // output word (MSB-first: row i at bit 63 - i)
-        if (oc < cols) out[oc * pout + ow] = __brevll(((u64)c0b << 32) | c0a);
-        if (oc + 32 < cols) out[(oc + 32) * pout + ow] = __brevll(((u64)c1b << 32) | c1a);
+        stg[64 * ww + lane][g] = __brevll(((u64)c0b << 32) | c0a);  // MSB-first: row i at bit 63 - i
+        stg[64 * ww + 32 + lane][g] = __brevll(((u64)c1b << 32) | c1a);
+    }
+    __syncthreads();
+    const int64_t ow0 = r0 / 64;
+    const bool vec = (pout % 2 == 0) && ((uintptr_t)out % 16 == 0);
+#pragma unroll
+    for (int i = 0; i < 64 * TR_WORDS * TR_OUT_WORDS / 2 / 256; ++i) {
+        const int idx = threadIdx.x + 256 * i;
+        const int orow = idx / (TR_OUT_WORDS / 2), ch = idx % (TR_OUT_WORDS / 2);
+        const int64_t oc = w0 * 64 + orow, ow = ow0 + 2 * ch;
+        if (oc >= cols || ow >= wrows) continue;
+        u64 *d = out + oc * pout + ow;
+        if (vec && ow + 1 < wrows) {
+            *reinterpret_cast<ulonglong2 *>(d) = make_ulonglong2(stg[orow][2 * ch], stg[orow][2 * ch + 1]);
+        } else {
+            d[0] = stg[orow][2 * ch];
+            if (ow + 1 < wrows) d[1] = stg[orow][2 * ch + 1];
+        }
     }
 }
 

@@ -1362,7 +1362,7 @@ int launch_umma_f4(const UmmaJob &jb, int64_t nprob, cudaStream_t s) {
         if (!jb.accumulate)
             for (int64_t q = 0; q < nprob && rc == GF2_OK; ++q) {
                 gf2_view v{jb.C + q * jb.sc, jb.pc, jb.m, jb.n};
-                rc = launch_ewise(v, nullptr, nullptr, 0, s);
+                rc = launch_zero(v, s);
             }
         ua.mode = 2;
     } else {
@@ -1413,7 +1413,7 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
         if (jb.accumulate || jb.fuse_post) return GF2_OK;
         for (int64_t q = 0; q < nprob; ++q) {
             gf2_view v{jb.C + q * jb.sc, jb.pc, jb.m, jb.n};
-            GF2_TRY(launch_ewise(v, nullptr, nullptr, 0, s));
+            GF2_TRY(launch_zero(v, s));
         }
         return GF2_OK;
     }
@@ -1551,7 +1551,7 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
         if (!jb.accumulate) {
             for (int64_t q = 0; q < nprob && rc == GF2_OK; ++q) {
                 gf2_view v{jb.C + q * jb.sc, jb.pc, jb.m, jb.n};
-                rc = launch_ewise(v, nullptr, nullptr, 0, s);
+                rc = launch_zero(v, s);
             }
         }
         ua.mode = 2;
