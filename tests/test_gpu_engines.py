@@ -18,6 +18,7 @@ def _engine_reset():
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
+    P.set_threads(P.max_threads())
     prev = g.get_engine()
     yield
     g.set_engine(prev)
@@ -112,3 +113,35 @@ def test_mul_m4rm_always_runs_m4rm():
     ms, ops, n = g._lib.timer_read()
     g._lib.timer_enable(False)
     assert n == 1 and ops == 200 * 300 * 100
+
+
+@pytest.mark.parametrize("engine", ["tc-f4", "tc-i8"])
+@pytest.mark.parametrize("cutoff", [2048, 4096, 16384])
+def test_cfg3_every_depth(engine, cutoff, digests):
+    """The 16384^3 product at recursion depths 3, 2 and 0 (the default
+    cutoff 8192 = depth 1 is in test_configs): exercises the one-pass
+    addition levels and, on tc-f4, the level-0 B pre-addition that writes
+    its outputs transposed."""
+    g.set_engine(engine)
+    a, b = g.random(16384, 16384, 31), g.random(16384, 16384, 32)
+    c = g.mul_strassen(a, b, g.MulParams(cutoff=cutoff, k=8))
+    assert O.digest(words(c)) == digests["cfg3"]
+
+
+@pytest.mark.parametrize("engine", ["tc-f4", "tc-i8"])
+def test_large_peeled_tensor_recursion_vs_port(engine):
+    """Odd sizes, depth 2 with peeling, tensor-core leaves (2240x2048x2112,
+    above the M4RM crossover), ragged column tiles and odd word counts in the
+    transposed pre-addition; product and C += A.B against the C port."""
+    g.set_engine(engine)
+    m, l, n = 9000, 8300, 8500
+    pa, pb = O.random(m, l, 61), O.random(l, n, 62)
+    want = P.mul_strassen(pa, pb, cutoff=2048).words
+    a, b = g.random(m, l, 61), g.random(l, n, 62)
+    got = g.mul_strassen(a, b, g.MulParams(cutoff=2048, k=8))
+    assert np.array_equal(words(got), want)
+    assert g.trailing_bits_clean(got)
+    c = g.random(m, n, 63)
+    c0 = words(c)
+    g.addmul(c, a, b, g.MulParams(cutoff=2048, k=8))
+    assert np.array_equal(words(c), c0 ^ want)
