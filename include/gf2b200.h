@@ -105,7 +105,8 @@ int gf2_mul(const gf2_view *c, const gf2_view *a, const gf2_view *b,
 
 /* strassen.py:257-282 `mul_strassen` (+ peel_split strassen.py:66-84,
  * schedule strassen.py:141-204, peel_fixup strassen.py:219-249):
- * Strassen-Winograd recursion above `cutoff` over an M4RM base case.
+ * Strassen-Winograd recursion above `cutoff` over the selected base-case
+ * engine (gf2_set_engine; small leaves always run M4RM).
  * accumulate = 1 gives C += A.B (cfg4/cfg5 addmul). */
 int gf2_strassen(const gf2_view *c, const gf2_view *a, const gf2_view *b,
                  int64_t cutoff, int k, int accumulate, void *stream);
@@ -133,15 +134,17 @@ int gf2_peel_split(int64_t m, int64_t l, int64_t n, int64_t cutoff,
  * for the bench's `gpu_launches`). */
 int64_t gf2_launch_count(void);
 
-/* Kernel timer for the roofline: while enabled, every M4RM launch is
- * bracketed by CUDA events recorded on the stream it runs on. Enabling
+/* Kernel timer for the roofline: while enabled, every product launch (M4RM
+ * or tensor-core GEMM) is bracketed by CUDA events recorded on the stream it
+ * runs on. Enabling
  * resets the accumulators. gf2_timer_read synchronizes the recorded events
  * and returns the summed kernel milliseconds, the algorithmic bit-ops
  * (m*l*n per product) those launches computed, and the launch count. */
 int gf2_timer_enable(int on);
 /* Engine for Strassen leaves, non-recursive gf2_strassen calls and gf2_mul,
  * process-wide: 0 = M4RM shared-memory Gray tables, 1 = tcgen05 kind::i8
- * (default: measured fastest), 2 = tcgen05 kind::f8f6f4 (e4m3 0/1).
+ * (u8 0/1), 2 = tcgen05 kind::f8f6f4 (e4m3 0/1), 3 = tcgen05 kind::mxf4
+ * (e2m1 nibbles, unit block scales; default: measured fastest).
  * gf2_m4rm always runs the M4RM kernel. Results are identical. */
 int gf2_set_engine(int engine);
 int gf2_get_engine(void);
