@@ -85,6 +85,14 @@ struct CombineArgs {
     int64_t nprob;
     int accumulate;
 };
+// Per-device side stream (non-blocking) with a fork and a join event, for
+// independent work that can overlap on the GPU (one user per call site at a
+// time: the host thread issues fork -> side work -> join in order).
+struct SideStream {
+    cudaStream_t s;
+    cudaEvent_t fork, join;
+};
+int side_stream(SideStream **out);
 int launch_combine(const CombineArgs &a, cudaStream_t s);
 int launch_combine_t(const CombineArgs &a, cudaStream_t s);  // 7 transposed pre-add outputs
 int pool_setup();
@@ -122,6 +130,7 @@ struct UmmaJob {
     int fuse_post, accumulate;
     unsigned maskA[7], maskB[7], maskC[7];
     int b_trans;      // B given transposed (rows n, cols l, pitch pb); kind 2 only
+    cudaEvent_t b_ready;  // if set: B's source is produced on another stream
 };
 int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s);
 // multiply engine for every product (gf2_set_engine): 0 M4RM, 1 tcgen05 i8, 2 tcgen05 f8, 3 tcgen05 mxf4

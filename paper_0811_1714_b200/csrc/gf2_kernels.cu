@@ -373,3 +373,20 @@ int launch_combine_t(const CombineArgs &a, cudaStream_t s) {
     return check_cuda(cudaGetLastError(), "k_combine_t launch");
 }
 }  // namespace gf2
+
+namespace gf2 {
+int side_stream(SideStream **out) {
+    static SideStream sides[64] = {};
+    int dev = 0;
+    GF2_TRY(check_cuda(cudaGetDevice(&dev), "cudaGetDevice"));
+    if (dev < 0 || dev >= 64) return set_error(GF2_ERR_CUDA, "device index out of range");
+    SideStream &sd = sides[dev];
+    if (!sd.s) {
+        GF2_TRY(check_cuda(cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking), "side stream"));
+        GF2_TRY(check_cuda(cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming), "fork event"));
+        GF2_TRY(check_cuda(cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming), "join event"));
+    }
+    *out = &sd;
+    return GF2_OK;
+}
+}  // namespace gf2

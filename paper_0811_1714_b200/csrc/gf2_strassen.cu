@@ -99,7 +99,18 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
     }
     int rc = GF2_OK;
     gf2_view Bt0{ws + offBt0, Lw[0], N[0], L[0]};
-    if (bt && lastA == 0) rc = launch_transpose(Bt0, B0, s);
+    // depth 1: transpose B0 on a side stream, overlapping the A-side
+    // expansion; only the B-side expansion waits for it (UmmaJob::b_ready)
+    cudaEvent_t bt_ready = nullptr;
+    if (bt && lastA == 0) {
+        SideStream *sd = nullptr;
+        rc = side_stream(&sd);
+        if (rc == GF2_OK) rc = check_cuda(cudaEventRecord(sd->fork, s), "fork");
+        if (rc == GF2_OK) rc = check_cuda(cudaStreamWaitEvent(sd->s, sd->fork, 0), "fork wait");
+        if (rc == GF2_OK) rc = launch_transpose(Bt0, B0, sd->s);
+        if (rc == GF2_OK) rc = check_cuda(cudaEventRecord(sd->join, sd->s), "join");
+        bt_ready = sd->join;
+    }
     for (int lv = 0; lv < lastA && rc == GF2_OK; ++lv) {
         for (int side = 0; side < 2 && rc == GF2_OK; ++side) {
             CombineArgs c{};
@@ -160,6 +171,7 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
             jb.sb = bt ? N[lastA] * Lw[lastA] : L[lastA] * Nw[lastA];
         }
         jb.b_trans = bt ? 1 : 0;
+        jb.b_ready = bt_ready;
         if (last == 0) {
             jb.C = C0.data; jb.pc = C0.pitch;
             if (!accumulate) rc = launch_zero(C0, s);
@@ -205,6 +217,7 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
         c.accumulate = lv == 0 ? accumulate : 0;
         rc = launch_combine(c, s);
     }
+    if (bt_ready) cudaStreamWaitEvent(s, bt_ready, 0);  // side work done before ws is released
     if (ws) cudaFreeAsync(ws, s);
     return rc;
 }

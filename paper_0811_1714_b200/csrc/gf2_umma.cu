@@ -1373,6 +1373,7 @@ int launch_umma_f4(const UmmaJob &jb, int64_t nprob, cudaStream_t s) {
         ea.q0 = eb.q0 = ua.q0 = q0;
         ua.nprob = nq;
         rc = launch_expand4(ea, nq, false, s);
+        if (rc == GF2_OK && jb.b_ready && q0 == 0) rc = check_cuda(cudaStreamWaitEvent(s, jb.b_ready, 0), "join wait");
         if (rc == GF2_OK) rc = launch_expand4(eb, nq, !bt, s);
         CUtensorMap ta, tb;
         if (rc == GF2_OK) rc = make_map(&ta, a4, (uint64_t)kb, (uint64_t)jb.m, (uint64_t)nq, kb, jb.m * kb);
