@@ -135,14 +135,16 @@ struct UmmaJob {
 int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s);
 // multiply engine for every product (gf2_set_engine): 0 M4RM, 1 tcgen05 i8, 2 tcgen05 f8, 3 tcgen05 mxf4
 extern int g_engine;
-// Products below ~2^34 bit-ops run faster on the M4RM kernel than through
-// byte expansion + tensor cores (fixed costs dominate; tools/bench_configs.py:
-// 1024^3 is 15 us on M4RM vs 113 us on tc-i8), so the automatic dispatch
-// (Strassen leaves, small non-recursive products) routes them there.
-constexpr double kTensorMinWork = 17179869184.0;  // 2^34
+// Products below ~1e10 bit-ops run faster on the M4RM kernel than through
+// operand expansion + tensor cores (fixed costs dominate). Measured with the
+// tc-f4 engine (tools/crossover.py): 2048^3 (8.6e9) 40 us M4RM vs 44 us tc-f4,
+// 2560^3 (1.7e10) 84 vs 53 us. The automatic dispatch (Strassen leaves,
+// small non-recursive products) routes by this total work. The 8-bit
+// engines move twice the operand bytes and cross over later (2^34).
+inline double tensor_min_work() { return g_engine == 3 ? 1.0e10 : 17179869184.0; }
 inline int launch_product(const M4rmBatch &b, cudaStream_t s) {
     const double work = (double)b.m * (double)b.l * (double)b.n * (double)b.nprob;
-    if (g_engine == 0 || work < kTensorMinWork) return launch_m4rm(b, s);
+    if (g_engine == 0 || work < tensor_min_work()) return launch_m4rm(b, s);
     return launch_umma(b, g_engine - 1, s);
 }
 int timer_enable(int on);

@@ -227,7 +227,7 @@ int strassen_core(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0, in
     if (g_engine != 0) {
         double leaf = (double)(A0.nrows >> depth) * (double)(A0.ncols >> depth) * (double)(B0.ncols >> depth);
         for (int i = 0; i < depth; ++i) leaf *= 7.0;
-        if (leaf >= kTensorMinWork) return strassen_core_tc(C0, A0, B0, depth, accumulate, s);
+        if (leaf >= tensor_min_work()) return strassen_core_tc(C0, A0, B0, depth, accumulate, s);
     }
     int64_t M[24], L[24], N[24], Lw[24], Nw[24], P[24];
     for (int i = 0; i <= depth; ++i) {
