@@ -908,6 +908,54 @@ __global__ void __launch_bounds__(256) k_expand4_rows(ExpandArgs a) {
     }
 }
 
+// Fused level, all 7 outputs of one source problem at once: a warp loads the
+// 4 quadrant words of 32 consecutive words x 4 rows ONCE, forms the 7
+// combinations (mask[i]) and writes each one's nibbles like k_expand4_rows
+// (output problem 7p + i). Quadrant words are read once instead of 14
+// times per 7 outputs.
+template <int ROWS>
+__global__ void __launch_bounds__(256) k_expand4_rows7(ExpandArgs a) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t width = words_per_row(a.cols);
+    const int64_t j0 = (int64_t)blockIdx.x * 32, j = j0 + lane;
+    const int64_t r0 = ((int64_t)blockIdx.y * 8 + warp) * ROWS;
+    if (r0 >= a.rows) return;
+    const u64 tm = (j == width - 1) ? tail_mask(a.cols) : ~0ULL;
+    const int64_t p = a.q0 / 7 + blockIdx.z;  // source problem
+    const u64 *s = a.src + p * a.sstride + j;
+    const bool live = j < width;
+    u64 qw[ROWS][4];
+#pragma unroll
+    for (int rr = 0; rr < ROWS; ++rr)
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            qw[rr][t] = (live && r0 + rr < a.rows) ? __ldg(s + a.qoff[t] + (r0 + rr) * a.sp) & tm : 0;
+    const int h = lane & 1;
+#pragma unroll 1
+    for (int i = 0; i < 7; ++i) {
+        const unsigned m = a.mask[i];
+        uint8_t *d = a.dst + ((int64_t)blockIdx.z * 7 + i) * a.dstride + j0 * 32;
+#pragma unroll
+        for (int rr = 0; rr < ROWS; ++rr) {
+            if (r0 + rr >= a.rows) break;
+            u64 x = 0;
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (m & (1u << t)) x ^= qw[rr][t];
+            x = __brevll(x);
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int wl = (lane >> 1) + 16 * k;
+                const u64 v = __shfl_sync(0xffffffffu, x, wl);
+                if (j0 + wl < width)
+                    *reinterpret_cast<uint4 *>(d + (r0 + rr) * a.dp + (lane + 32 * k) * 16) =
+                        make_uint4(nib_word(v, 4 * h), nib_word(v, 4 * h + 1), nib_word(v, 4 * h + 2),
+                                   nib_word(v, 4 * h + 3));
+            }
+        }
+    }
+}
+
 // B side, transposed. A block stages 256 K rows x 16 words (coalesced 128 B
 // row segments, fused quadrant XORs) in shared memory; each warp then owns
 // 2 words: per 64-row K block, four warp-wide 32 x 32 transposes turn the
@@ -1268,6 +1316,12 @@ int launch_expand(const ExpandArgs &a, int64_t nprob, cudaStream_t s) {
 int launch_expand4(const ExpandArgs &a, int64_t nprob, bool cols, cudaStream_t s) {
     const int64_t width = words_per_row(a.cols);
     if (!a.rows || !width || !nprob) return GF2_OK;
+    if (!cols && a.levels == 1 && a.q0 % 7 == 0 && nprob % 7 == 0) {
+        dim3 grd((unsigned)((width + 31) / 32), (unsigned)((a.rows + 8 * 4 - 1) / (8 * 4)), (unsigned)(nprob / 7));
+        k_expand4_rows7<4><<<grd, 256, 0, s>>>(a);
+        note_launch();
+        return check_cuda(cudaGetLastError(), "k_expand4_rows7 launch");
+    }
     if (!cols) {
         dim3 grd((unsigned)((width + 31) / 32), (unsigned)((a.rows + 8 * F4_ROWS_PER_WARP - 1) / (8 * F4_ROWS_PER_WARP)),
                  (unsigned)nprob);
@@ -1315,7 +1369,8 @@ int launch_umma_f4(const UmmaJob &jb, int64_t nprob, cudaStream_t s) {
     const int64_t np = (jb.n + 63) / 64 * 64;   // B rows (columns of B), whole words
     const int64_t per = jb.m * kb + np * kb;
     const int64_t cap = (int64_t)8 << 30;
-    const int64_t qchunk = std::max<int64_t>(1, std::min<int64_t>(nprob, cap / std::max<int64_t>(per, 1)));
+    int64_t qchunk = std::max<int64_t>(1, std::min<int64_t>(nprob, cap / std::max<int64_t>(per, 1)));
+    if (jb.fuse_pre == 1 && qchunk >= 7) qchunk -= qchunk % 7;  // whole 7-product groups (k_expand4_rows7)
     uint8_t *ws = nullptr;
     GF2_TRY(pool_setup());
     cudaError_t e = cudaMallocAsync((void **)&ws, (size_t)(qchunk * per), s);
