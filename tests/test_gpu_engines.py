@@ -145,3 +145,36 @@ def test_large_peeled_tensor_recursion_vs_port(engine):
     c0 = words(c)
     g.addmul(c, a, b, g.MulParams(cutoff=2048, k=8))
     assert np.array_equal(words(c), c0 ^ want)
+
+
+@pytest.mark.parametrize("engine", ["tc-f4", "tc-i8"])
+def test_tensor_recursion_on_windows_vs_port(engine):
+    """Windows (odd word offsets, pitch != width) through the tensor-core
+    recursion: depth 1 at cutoff 2048 with FP4/i8 leaves; product into a
+    fresh matrix and C += A.B into a window of a larger C, whose bits
+    outside the window must not change."""
+    g.set_engine(engine)
+    pa, pb, pc = g.random(5200, 4700, 71), g.random(4700, 5000, 72), g.random(5300, 5100, 73)
+    aw = g.window(pa, 37, 64, 5100, 4500)          # word offset 1
+    bw = g.window(pb, 101, 192, 4500, 4700)        # word offset 3
+    cw = g.window(pc, 55, 128, 5100, 4700)         # word offset 2
+    ha, hb = words(pa), words(pb)
+    sub_a = O.HostMat(5100, 4500, np.ascontiguousarray(ha[37:37 + 5100, 1:1 + 71]))
+    sub_b = O.HostMat(4500, 4700, np.ascontiguousarray(hb[101:101 + 4500, 3:3 + 74]))
+    sub_a.words[:, -1] &= np.uint64(O.tail_mask(4500))
+    sub_b.words[:, -1] &= np.uint64(O.tail_mask(4700))
+    want = P.mul_strassen(sub_a, sub_b, cutoff=2048).words
+    got = g.mul_strassen(aw, bw, g.MulParams(cutoff=2048, k=8))
+    assert np.array_equal(words(got), want)
+    before = words(pc).copy()
+    g.addmul(cw, aw, bw, g.MulParams(cutoff=2048, k=8))
+    after = words(pc)
+    region = before[55:55 + 5100, 2:2 + 74].copy()
+    # the window's last word holds 4700 - 73*64 = 28 columns; bits past them belong to the parent
+    keep = np.uint64(~O.tail_mask(4700) & 0xFFFFFFFFFFFFFFFF)
+    exp = region ^ want
+    exp[:, -1] = (exp[:, -1] & ~keep) | (region[:, -1] & keep)
+    assert np.array_equal(after[55:55 + 5100, 2:2 + 74], exp)
+    outside = before.copy()
+    outside[55:55 + 5100, 2:2 + 74] = after[55:55 + 5100, 2:2 + 74]
+    assert np.array_equal(after, outside)
