@@ -178,3 +178,29 @@ def test_tensor_recursion_on_windows_vs_port(engine):
     outside = before.copy()
     outside[55:55 + 5100, 2:2 + 74] = after[55:55 + 5100, 2:2 + 74]
     assert np.array_equal(after, outside)
+
+
+def test_f4_direct_random_windows_vs_port():
+    """tc-f4 single products (no recursion: transposing B expansion, several
+    row and column tiles, ragged tile widths) on random shapes and window
+    offsets, plain and accumulating into a window."""
+    g.set_engine("tc-f4")
+    rng = np.random.default_rng(17)
+    for trial in range(6):
+        m, l, n = (int(x) for x in rng.integers(300, 2600, 3))
+        ra, ca, rb, cb = (int(x) for x in rng.integers(0, 4, 4))
+        pa = g.random(m + ra + 3, l + 64 * ca + 70, 100 + trial)
+        pb = g.random(l + rb + 5, n + 64 * cb + 90, 200 + trial)
+        aw, bw = g.window(pa, ra, 64 * ca, m, l), g.window(pb, rb, 64 * cb, l, n)
+        wa, wb = words(pa), words(pb)
+        sa = np.ascontiguousarray(wa[ra:ra + m, ca:ca + O.words_per_row(l)])
+        sb = np.ascontiguousarray(wb[rb:rb + l, cb:cb + O.words_per_row(n)])
+        sa[:, -1] &= np.uint64(O.tail_mask(l))
+        sb[:, -1] &= np.uint64(O.tail_mask(n))
+        want = P.mul_strassen(O.HostMat(m, l, sa), O.HostMat(l, n, sb), cutoff=64).words
+        got = g.mul_direct(aw, bw)
+        assert np.array_equal(words(got), want), (m, l, n)
+        c = g.random(m, n, 300 + trial)
+        c0 = words(c)
+        g.addmul_direct(c, aw, bw)
+        assert np.array_equal(words(c), c0 ^ want), (m, l, n)
