@@ -1,5 +1,6 @@
 // Internal declarations shared by the gf2b200 translation units.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -147,6 +148,11 @@ inline int launch_product(const M4rmBatch &b, cudaStream_t s) {
     if (g_engine == 0 || work < tensor_min_work()) return launch_m4rm(b, s);
     return launch_umma(b, g_engine - 1, s);
 }
+// cuTensorMapEncodeTiled through the runtime's driver entry point: a 3-D
+// map (inner, outer, problems), byte strides for dims 1 and 2, no
+// interleave, 128-byte swizzle or none, OOB elements read as zero.
+int encode_map_3d(CUtensorMap *map, CUtensorMapDataType dt, void *base, const uint64_t dims[3],
+                  const uint64_t strides[2], const uint32_t box[3], bool swizzle128);
 int timer_enable(int on);
 int timer_begin(cudaStream_t s, double bitops);  // -1 when the timer is off
 void timer_end(int idx, cudaStream_t s);

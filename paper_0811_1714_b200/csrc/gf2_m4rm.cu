@@ -51,7 +51,7 @@ constexpr int kBStageBytes = kStageRows * kRowBytes;  // 16 KiB
 
 template <int RPT>
 constexpr int smem_bytes() {
-    return kTables * kTableBytes + 2 * kBStageBytes + 2 * (kRowGroups * RPT) * 8 * kStageWords;
+    return kTables * kTableBytes + 2 * kBStageBytes + 2 * (kRowGroups * RPT) * 8 * kStageWords + 16;
 }
 
 struct KArgs {
@@ -78,6 +78,28 @@ __device__ __forceinline__ void cp_async(uint32_t saddr, const void *g, int byte
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(g), "r"(bytes)
                      : "memory");
 }
+__device__ __forceinline__ void mbar_init1(uint32_t bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(dst),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
@@ -93,15 +115,20 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
     return v;
 }
 
-// C tile: BM = 64*RPT rows x 1024 columns, in registers. ALIGN16: operands
-// allow 16-byte cp.async (base and pitch 16-byte aligned).
-template <int RPT, bool ALIGN16>
-__global__ void __launch_bounds__(kThreads, 1) k_m4rm(KArgs p) {
+// C tile: BM = 64*RPT rows x 1024 columns, in registers. TMA: operands are
+// 16-byte aligned with 16-byte pitches, so thread 0 stages each B panel
+// (128 rows x 16 words) and the A words (BM rows x 2 words, 256-row boxes)
+// with cp.async.bulk.tensor onto one mbarrier per buffer (zero fill past the
+// matrix edges); otherwise every thread issues 8-byte cp.async.
+template <int RPT, bool TMA>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_m4rm(KArgs p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
     constexpr int BM = kRowGroups * RPT;
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t s_tab = (uint32_t)__cvta_generic_to_shared(smem);
     const uint32_t s_bst = s_tab + kTables * kTableBytes;
     const uint32_t s_ast = s_bst + 2 * kBStageBytes;
+    const uint32_t s_bar = s_ast + 2 * BM * 16;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -128,46 +155,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_m4rm(KArgs p) {
     // stage = A words [kw, kw+2) of BM rows and the 128 matching rows of B
     auto load_stage = [&](int64_t kw, int buf) {
         const uint32_t bdst = s_bst + buf * kBStageBytes;
-        if (ALIGN16) {
+        if (TMA) {
+            if (tid == 0) {
+                const uint32_t bar = s_bar + 8 * buf;
+                mbar_expect(bar, kBStageBytes + BM * 16);
+                tma_3d(bdst, &tmB, (int)col_w0, (int)(kw * 64), (int)prob, bar);
 #pragma unroll
-            for (int i = 0; i < (kStageRows * kTileWords / 2) / kThreads; ++i) {
-                const int e = tid + kThreads * i;
-                const int r = e >> 3, c2 = (e & 7) * 2;
-                const int64_t brow = kw * 64 + r;
-                const int64_t wv = p.Wn - (col_w0 + c2);
-                const int bytes = (brow < p.l) ? (wv >= 2 ? 16 : (wv == 1 ? 8 : 0)) : 0;
-                const u64 *src = bytes ? (B + brow * p.pb + col_w0 + c2) : B;
-                cp_async<16>(bdst + r * kRowBytes + c2 * 8, src, bytes);
+                for (int i = 0; i < BM / 256; ++i)
+                    tma_3d(s_ast + (buf * BM + 256 * i) * 16, &tmA, (int)kw, (int)(row0 + 256 * i), (int)prob, bar);
             }
+            return;
+        }
 #pragma unroll
-            for (int i = 0; i < (BM + kThreads - 1) / kThreads; ++i) {
-                const int r = tid + kThreads * i;
-                if (r < BM) {
-                    const int64_t wv = kw1 - kw;
-                    const int bytes = (row0 + r < p.m) ? (wv >= 2 ? 16 : 8) : 0;
-                    const u64 *src = bytes ? (A + (row0 + r) * p.pa + kw) : A;
-                    cp_async<16>(s_ast + (buf * BM + r) * 16, src, bytes);
-                }
-            }
-        } else {
+        for (int i = 0; i < (kStageRows * kTileWords) / kThreads; ++i) {
+            const int e = tid + kThreads * i;
+            const int r = e >> 4, wd = e & 15;
+            const int64_t brow = kw * 64 + r;
+            const bool ok = (brow < p.l) && (col_w0 + wd < p.Wn);
+            const u64 *src = ok ? (B + brow * p.pb + col_w0 + wd) : B;
+            cp_async<8>(bdst + r * kRowBytes + wd * 8, src, ok ? 8 : 0);
+        }
 #pragma unroll
-            for (int i = 0; i < (kStageRows * kTileWords) / kThreads; ++i) {
-                const int e = tid + kThreads * i;
-                const int r = e >> 4, wd = e & 15;
-                const int64_t brow = kw * 64 + r;
-                const bool ok = (brow < p.l) && (col_w0 + wd < p.Wn);
-                const u64 *src = ok ? (B + brow * p.pb + col_w0 + wd) : B;
-                cp_async<8>(bdst + r * kRowBytes + wd * 8, src, ok ? 8 : 0);
-            }
-#pragma unroll
-            for (int i = 0; i < (2 * BM + kThreads - 1) / kThreads; ++i) {
-                const int e = tid + kThreads * i;
-                if (e < 2 * BM) {
-                    const int r = e >> 1, wd = e & 1;
-                    const bool ok = (row0 + r < p.m) && (kw + wd < kw1);
-                    const u64 *src = ok ? (A + (row0 + r) * p.pa + kw + wd) : A;
-                    cp_async<8>(s_ast + (buf * BM + r) * 16 + wd * 8, src, ok ? 8 : 0);
-                }
+        for (int i = 0; i < (2 * BM + kThreads - 1) / kThreads; ++i) {
+            const int e = tid + kThreads * i;
+            if (e < 2 * BM) {
+                const int r = e >> 1, wd = e & 1;
+                const bool ok = (row0 + r < p.m) && (kw + wd < kw1);
+                const u64 *src = ok ? (A + (row0 + r) * p.pa + kw + wd) : A;
+                cp_async<8>(s_ast + (buf * BM + r) * 16 + wd * 8, src, ok ? 8 : 0);
             }
         }
         cp_async_commit();
@@ -180,10 +195,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_m4rm(KArgs p) {
     // table-build role: table tj, slots [r0*16, r0*16+16), slice s
     const int tj = rg >> 4, r0 = rg & 15;
 
+    if (TMA) {
+        if (tid == 0) {
+            mbar_init1(s_bar);
+            mbar_init1(s_bar + 8);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+    }
     if (kw0 < kw1) load_stage(kw0, 0);
     int buf = 0;
-    for (int64_t kw = kw0; kw < kw1; kw += kStageWords, buf ^= 1) {
-        cp_async_wait_all();
+    uint32_t it = 0;
+    for (int64_t kw = kw0; kw < kw1; kw += kStageWords, buf ^= 1, ++it) {
+        if (TMA)
+            mbar_wait_parity(s_bar + 8 * buf, (it >> 1) & 1);
+        else
+            cp_async_wait_all();
         __syncthreads();  // stage visible; previous lookups finished
         if (kw + kStageWords < kw1) load_stage(kw + kStageWords, buf ^ 1);
         const int nhalf = (kw + 1 < kw1) ? 4 : 2;
@@ -265,17 +292,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_m4rm(KArgs p) {
     }
 }
 
-template <int RPT, bool A16>
-int launch_rpt(const KArgs &ka, int64_t col_tiles, int64_t row_tiles, int64_t zdim, cudaStream_t s) {
+template <int RPT, bool TMA>
+int launch_rpt(const KArgs &ka, const CUtensorMap &ta, const CUtensorMap &tb, int64_t col_tiles, int64_t row_tiles,
+               int64_t zdim, cudaStream_t s) {
     static bool configured = false;
     constexpr int sm = smem_bytes<RPT>();
     if (!configured) {
-        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_m4rm<RPT, A16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_m4rm<RPT, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
                            "cudaFuncSetAttribute(k_m4rm)"));
         configured = true;
     }
     dim3 grid((unsigned)col_tiles, (unsigned)row_tiles, (unsigned)zdim);
-    k_m4rm<RPT, A16><<<grid, kThreads, sm, s>>>(ka);
+    k_m4rm<RPT, TMA><<<grid, kThreads, sm, s>>>(ka, ta, tb);
     note_launch();
     return check_cuda(cudaGetLastError(), "k_m4rm launch");
 }
@@ -393,18 +421,30 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     }
     const int64_t z = (int64_t)nsplit * b.nprob;
     const int tidx = timer_begin(s, (double)b.m * (double)b.l * (double)b.n * (double)b.nprob);
-    const bool a16 = ((uintptr_t)b.A % 16 == 0) && ((uintptr_t)b.B % 16 == 0) && (b.pa % 2 == 0) &&
-                     (b.pb % 2 == 0) && (b.nprob == 1 || (b.sa % 2 == 0 && b.sb % 2 == 0));
+    bool tma = ((uintptr_t)b.A % 16 == 0) && ((uintptr_t)b.B % 16 == 0) && (b.pa % 2 == 0) && (b.pb % 2 == 0) &&
+               (b.nprob == 1 || (b.sa % 2 == 0 && b.sb % 2 == 0));
+    CUtensorMap ta{}, tb{};
+    if (tma) {
+        // words x rows x problems; the problem stride is unused when nprob == 1
+        const uint64_t da[3] = {(uint64_t)Wl, (uint64_t)b.m, (uint64_t)b.nprob};
+        const uint64_t sa[2] = {(uint64_t)b.pa * 8, (uint64_t)(b.nprob > 1 ? b.sa : b.m * b.pa) * 8};
+        const uint32_t ba[3] = {2, 256, 1};
+        const uint64_t db[3] = {(uint64_t)Wn, (uint64_t)b.l, (uint64_t)b.nprob};
+        const uint64_t sb[2] = {(uint64_t)b.pb * 8, (uint64_t)(b.nprob > 1 ? b.sb : b.l * b.pb) * 8};
+        const uint32_t bb[3] = {(uint32_t)kTileWords, (uint32_t)kStageRows, 1};
+        tma = encode_map_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT64, (void *)b.A, da, sa, ba, false) == GF2_OK &&
+              encode_map_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT64, (void *)b.B, db, sb, bb, false) == GF2_OK;
+    }
     int rc;
     if (rpt == 16)
-        rc = a16 ? launch_rpt<16, true>(ka, col_tiles, row_tiles, z, s)
-                 : launch_rpt<16, false>(ka, col_tiles, row_tiles, z, s);
+        rc = tma ? launch_rpt<16, true>(ka, ta, tb, col_tiles, row_tiles, z, s)
+                 : launch_rpt<16, false>(ka, ta, tb, col_tiles, row_tiles, z, s);
     else if (rpt == 8)
-        rc = a16 ? launch_rpt<8, true>(ka, col_tiles, row_tiles, z, s)
-                 : launch_rpt<8, false>(ka, col_tiles, row_tiles, z, s);
+        rc = tma ? launch_rpt<8, true>(ka, ta, tb, col_tiles, row_tiles, z, s)
+                 : launch_rpt<8, false>(ka, ta, tb, col_tiles, row_tiles, z, s);
     else
-        rc = a16 ? launch_rpt<4, true>(ka, col_tiles, row_tiles, z, s)
-                 : launch_rpt<4, false>(ka, col_tiles, row_tiles, z, s);
+        rc = tma ? launch_rpt<4, true>(ka, ta, tb, col_tiles, row_tiles, z, s)
+                 : launch_rpt<4, false>(ka, ta, tb, col_tiles, row_tiles, z, s);
     timer_end(tidx, s);
     return rc;
 }

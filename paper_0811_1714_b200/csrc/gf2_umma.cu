@@ -1297,6 +1297,20 @@ int g_sms = 0;
 
 }  // namespace
 
+int encode_map_3d(CUtensorMap *map, CUtensorMapDataType dt, void *base, const uint64_t dims[3],
+                  const uint64_t strides[2], const uint32_t box[3], bool swizzle128) {
+    GF2_TRY(get_encode());
+    cuuint64_t d[3] = {dims[0], dims[1], dims[2]};
+    cuuint64_t st[2] = {strides[0], strides[1]};
+    cuuint32_t bx[3] = {box[0], box[1], box[2]};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = g_encode(map, dt, 3, base, d, st, bx, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(GF2_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return GF2_OK;
+}
+
 int launch_expand(const ExpandArgs &a, int64_t nprob, cudaStream_t s) {
     const int64_t width = words_per_row(a.cols);
     if (!a.rows || !width || !nprob) return GF2_OK;
