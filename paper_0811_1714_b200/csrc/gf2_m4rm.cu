@@ -400,11 +400,22 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
         row_tiles = (b.m + kRowGroups * rpt - 1) / (kRowGroups * rpt);
     }
     const int64_t tiles = row_tiles * col_tiles * b.nprob;
+    // split K so the CTA count fills whole waves of resident CTAs (one per
+    // SM): efficiency(n) = T n / (S ceil(T n / S)). A split costs a zeroing
+    // pass and red.xor accumulation, hence the small penalty. (16384^3:
+    // 256 tiles -> 1.73 waves at n = 1, 6.92 waves / 98.8 % at n = 4.)
+    auto wave_eff = [&](int64_t n) {
+        const int64_t ctas = tiles * n;
+        return (double)ctas / (double)(want * ((ctas + want - 1) / want));
+    };
     int nsplit = 1;
-    if (tiles < want) {
-        int64_t ns = (want + tiles - 1) / tiles;
-        if (ns > Wl) ns = Wl;
-        nsplit = (int)ns;
+    double best = wave_eff(1);
+    for (int64_t n = 2; n <= 8 && n <= (Wl + 1) / 2; ++n) {
+        const double e = wave_eff(n) - 0.02;
+        if (e > best + 1e-9) {
+            best = e;
+            nsplit = (int)n;
+        }
     }
     int64_t kws = (Wl + nsplit - 1) / nsplit;
     kws = (kws + kStageWords - 1) / kStageWords * kStageWords;  // splits start on a stage
