@@ -56,63 +56,105 @@ def parse():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled DURING the timed region: NVML
+    polled every millisecond (the device matched by PCI bus id), falling
+    back to `nvidia-smi -lms 100` if NVML is unavailable. Reports the median
+    and minimum SM clock under load and every throttle reason seen."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+             "sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
+        self.samples = []          # (sm_mhz, set of reasons)
+        self.max_mhz = None
+        self.stop_flag = threading.Event()
+        self.mode = None
         self.proc = None
-        self.lines = []
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        try:
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index),
-                 f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE,
-                stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
+            nv, h = self._nvml_handle()
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            def loop():
+                while not self.stop_flag.is_set():
+                    try:
+                        mhz = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((mhz, {k for k, v in bits.items() if r & v}))
+                    except Exception:
+                        pass
+                    time.sleep(0.001)
+            self.t = threading.Thread(target=loop, daemon=True)
+            self.t.start()
+            self.mode = "nvml"
+            return
+        except Exception:
+            pass
+        try:
+            fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                      "clocks_event_reasons.hw_thermal_slowdown,"
+                      "clocks_event_reasons.sw_thermal_slowdown,"
+                      "clocks_event_reasons.sw_power_cap")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={fields}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+
+            def read():
+                for line in self.proc.stdout:
+                    f = [x.strip() for x in line.split(",")]
+                    if len(f) < 6:
+                        continue
+                    try:
+                        mhz, self.max_mhz = float(f[0]), float(f[1])
+                    except ValueError:
+                        continue
+                    self.samples.append((mhz, {n for n, v in zip(self.NAMES, f[2:6])
+                                               if v.lower().startswith("active")}))
+            self.t = threading.Thread(target=read, daemon=True)
+            self.t.start()
+            self.mode = "nvidia-smi"
+        except Exception:
+            self.mode = None
 
     def stop(self):
-        if self.proc is None:
+        if self.mode is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
-                 "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 8:
-                continue
+        if self.mode == "nvml":
+            self.stop_flag.set()
+            self.t.join(timeout=2)
+        else:
+            time.sleep(0.25)
+            self.proc.terminate()
             try:
-                sm.append(float(f[0]))
-                mx = float(f[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[4:8]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        sm.sort()
-        med = sm[len(sm) // 2] if sm else None
-        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        sm = sorted(x[0] for x in self.samples)
+        reasons = set()
+        for _, r in self.samples:
+            reasons |= r
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_min_mhz": sm[0] if sm else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+                "samples": len(sm), "source": self.mode}
 
 
 def measured_peaks():
@@ -262,6 +304,8 @@ def main():
         c = step()
         e1.record(stream)
         evs.append((e0, e1))
+    while not evs[-1][1].query():          # wait without holding the GIL, so the
+        time.sleep(0.0002)                 # clock sampler thread keeps sampling
     torch.cuda.synchronize()
     n_launch = g.launch_count() - n_launch0
     kern_ms, kern_ops, kern_n = _lib.timer_read()
