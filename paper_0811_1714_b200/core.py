@@ -12,6 +12,8 @@ column offsets; writes through them keep the bits beyond their right edge.
 
 from __future__ import annotations
 
+import sys
+
 import numpy as np
 
 from . import _lib
@@ -94,7 +96,7 @@ class BitMatrix:
         return _download(self, out)
 
     def to_host(self):
-        return HostMatrix(self.nrows, self.ncols, self.to_numpy())
+        return _to_host(self)
 
     def __eq__(self, other) -> bool:
         if not isinstance(other, (BitMatrix, MatrixWindow)):
@@ -163,7 +165,7 @@ class MatrixWindow:
         return _download(self, out)
 
     def to_host(self):
-        return HostMatrix(self.nrows, self.ncols, self.to_numpy())
+        return _to_host(self)
 
     def __eq__(self, other) -> bool:
         if not isinstance(other, (BitMatrix, MatrixWindow)):
@@ -206,6 +208,21 @@ class HostMatrix:
     @property
     def shape(self):
         return (self.nrows, self.ncols)
+
+
+def _to_host(m):
+    """Owned host copy: a real `gf2mat.BitMatrix` (core.py:57-82, built with
+    gf2mat.create and filled through its `words` view) when the caller has
+    imported the reference package, else a HostMatrix with the same
+    attribute surface. This package never imports gf2mat itself."""
+    words = m.to_numpy()
+    ref = sys.modules.get("gf2mat")
+    if ref is not None and hasattr(ref, "create"):
+        out = ref.create(m.nrows, m.ncols)
+        if m.nrows and words.shape[1]:
+            out.words[:, :] = words
+        return out
+    return HostMatrix(m.nrows, m.ncols, words)
 
 
 def _stream():

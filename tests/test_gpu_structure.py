@@ -91,3 +91,31 @@ def test_gf2m_roundtrip_and_reference_bytes(golden, tmp_path):
     big = g.random(3000, 4097, 9)
     g.save(big, fp)
     assert g.equal(g.load(fp), big)
+
+
+def test_to_host_returns_reference_matrix_when_gf2mat_is_imported(monkeypatch):
+    """to_host() hands back the reference's own BitMatrix type
+    when the caller has gf2mat imported (stand-in module here: the
+    reference is not present on the GPU box), else a HostMatrix."""
+    import sys
+    import types
+
+    class StubBitMatrix:  # the reference's constructor shape (core.py:71-80)
+        def __init__(self, nrows, ncols):
+            self.nrows, self.ncols = nrows, ncols
+            self.width = (ncols + 63) // 64
+            self.data = np.zeros(nrows * self.width, dtype=np.uint64)
+            self.words = self.data.reshape(nrows, self.width)
+
+    stub = types.ModuleType("gf2mat")
+    stub.create = StubBitMatrix
+    monkeypatch.setitem(sys.modules, "gf2mat", stub)
+    a = g.random(100, 130, 5)
+    h = a.to_host()
+    assert isinstance(h, StubBitMatrix)
+    assert np.array_equal(h.words, a.to_numpy())
+    w = g.window(a, 3, 64, 50, 66)
+    hw = w.to_host()
+    assert isinstance(hw, StubBitMatrix) and np.array_equal(hw.words, w.to_numpy())
+    monkeypatch.delitem(sys.modules, "gf2mat")
+    assert isinstance(a.to_host(), g.HostMatrix)
