@@ -204,3 +204,28 @@ def test_f4_direct_random_windows_vs_port():
         c0 = words(c)
         g.addmul_direct(c, aw, bw)
         assert np.array_equal(words(c), c0 ^ want), (m, l, n)
+
+
+@pytest.mark.parametrize("engine", ["tc-f4", "tc-i8"])
+def test_two_fused_levels_option(engine, digests):
+    """GF2_FUSE_LEVELS=2 (read once per process, hence a subprocess): both
+    Strassen levels of a depth-2 product folded into the operand expansion
+    (up to 16 source blocks per word; on tc-f4 the B side gathers from B^T
+    with swapped quadrant masks at both levels)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import paper_0811_1714_b200 as g\n"
+        "from oracle import gf2_oracle as O\n"
+        "g.set_engine(%r)\n"
+        "a, b = g.random(16384, 16384, 31), g.random(16384, 16384, 32)\n"
+        "print(O.digest(g.mul_strassen(a, b, g.MulParams(cutoff=4096)).to_numpy()))\n"
+    ) % (root, engine)
+    env = dict(os.environ, GF2_FUSE_LEVELS="2")
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root,
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.strip().splitlines()[-1] == digests["cfg3"]
