@@ -52,6 +52,11 @@ enum {
 const char *gf2_version(void);
 const char *gf2_last_error(void);
 
+/* Wait for all work queued on `stream` (NULL: the whole device). The
+ * library links the CUDA runtime statically, so hosts that do not use CUDA
+ * themselves synchronize through this call. */
+int gf2_stream_sync(void *stream);
+
 /* Recommended row pitch (words) for an owned device matrix of ncols
  * columns: 16-byte multiple, 128-byte multiple once a row spans 16 words. */
 int64_t gf2_pitch_words(int64_t ncols);

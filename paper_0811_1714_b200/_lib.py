@@ -65,6 +65,7 @@ SIGNATURES = {
                        + [ctypes.POINTER(ctypes.c_int64)]),
     "gf2_launch_count": (ctypes.c_int64, []),
     "gf2_timer_enable": (ctypes.c_int, [ctypes.c_int]),
+    "gf2_stream_sync": (ctypes.c_int, [ctypes.c_void_p]),
     "gf2_set_engine": (ctypes.c_int, [ctypes.c_int]),
     "gf2_get_engine": (ctypes.c_int, []),
     "gf2_timer_read": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double),

@@ -88,6 +88,11 @@ const char *gf2_version(void) { return "gf2b200 0.1.0 (sm_100a)"; }
 
 const char *gf2_last_error(void) { return t_err.c_str(); }
 
+int gf2_stream_sync(void *stream) {
+    if (!stream) return check_cuda(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    return check_cuda(cudaStreamSynchronize((cudaStream_t)stream), "cudaStreamSynchronize");
+}
+
 int64_t gf2_pitch_words(int64_t ncols) {
     int64_t w = words_per_row(ncols);
     if (w >= 16) return (w + 15) / 16 * 16;
