@@ -14,7 +14,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 from . import _lib
-from .core import BitMatrix, Mat, _check_cuda_dev, _stream, create
+from .core import BitMatrix, Mat, _check_cuda_dev, _stream
 from .errors import DimensionError, ParameterError
 
 MAX_K = 16

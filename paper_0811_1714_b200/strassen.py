@@ -14,7 +14,7 @@ from dataclasses import dataclass
 from typing import NamedTuple
 
 from . import _lib
-from .core import BitMatrix, Mat, _check_cuda_dev, _stream, create
+from .core import BitMatrix, Mat, _check_cuda_dev, _stream
 from .errors import DimensionError, ParameterError
 
 _WORD = 64
