@@ -164,28 +164,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int i = 0; i < BM / 256; ++i)
                     tma_3d(s_ast + (buf * BM + 256 * i) * 16, &tmA, (int)kw, (int)(row0 + 256 * i), (int)prob, bar);
             }
-            return;
-        }
+        } else {
 #pragma unroll
-        for (int i = 0; i < (kStageRows * kTileWords) / kThreads; ++i) {
-            const int e = tid + kThreads * i;
-            const int r = e >> 4, wd = e & 15;
-            const int64_t brow = kw * 64 + r;
-            const bool ok = (brow < p.l) && (col_w0 + wd < p.Wn);
-            const u64 *src = ok ? (B + brow * p.pb + col_w0 + wd) : B;
-            cp_async<8>(bdst + r * kRowBytes + wd * 8, src, ok ? 8 : 0);
-        }
-#pragma unroll
-        for (int i = 0; i < (2 * BM + kThreads - 1) / kThreads; ++i) {
-            const int e = tid + kThreads * i;
-            if (e < 2 * BM) {
-                const int r = e >> 1, wd = e & 1;
-                const bool ok = (row0 + r < p.m) && (kw + wd < kw1);
-                const u64 *src = ok ? (A + (row0 + r) * p.pa + kw + wd) : A;
-                cp_async<8>(s_ast + (buf * BM + r) * 16 + wd * 8, src, ok ? 8 : 0);
+            for (int i = 0; i < (kStageRows * kTileWords) / kThreads; ++i) {
+                const int e = tid + kThreads * i;
+                const int r = e >> 4, wd = e & 15;
+                const int64_t brow = kw * 64 + r;
+                const bool ok = (brow < p.l) && (col_w0 + wd < p.Wn);
+                const u64 *src = ok ? (B + brow * p.pb + col_w0 + wd) : B;
+                cp_async<8>(bdst + r * kRowBytes + wd * 8, src, ok ? 8 : 0);
             }
+#pragma unroll
+            for (int i = 0; i < (2 * BM + kThreads - 1) / kThreads; ++i) {
+                const int e = tid + kThreads * i;
+                if (e < 2 * BM) {
+                    const int r = e >> 1, wd = e & 1;
+                    const bool ok = (row0 + r < p.m) && (kw + wd < kw1);
+                    const u64 *src = ok ? (A + (row0 + r) * p.pa + kw + wd) : A;
+                    cp_async<8>(s_ast + (buf * BM + r) * 16 + wd * 8, src, ok ? 8 : 0);
+                }
+            }
+            cp_async_commit();
         }
-        cp_async_commit();
     };
 
     u64 acc[RPT][2];

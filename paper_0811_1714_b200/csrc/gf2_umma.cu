@@ -33,10 +33,6 @@ namespace gf2 {
 namespace {
 
 constexpr int BM = 128, BN = 256, BK = 128;
-constexpr int STAGES = 4;
-constexpr int A_STAGE = BM * BK;          // 16 KiB
-constexpr int B_STAGE = BN * BK;          // 32 KiB
-constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
 constexpr int UMMA_THREADS = 256;
 constexpr int64_t F8_KCHUNK = 8192;
 
@@ -106,10 +102,6 @@ __device__ __forceinline__ bool elect_one() {
     return pred != 0;
 }
 
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
-                 : "memory");
-}
 
 #define TMEM_LD32(taddr, r)                                                                                    \
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"  \
