@@ -5,9 +5,11 @@
 
 One JSON line on rank 0. Workload (BASELINE.json configs[2], the shape the
 metric is quoted on): C = A.B over GF(2), A and B 16384 x 16384 seeded
-splitmix64 bits (core.random seeds 31 / 32), Strassen-Winograd over M4RM.
-N = 1: one GPU multiplies. N > 1 (torchrun): C and A row-sharded, B
-broadcast from rank 0 over NVLink (NCCL) in K-panels inside the timed step.
+splitmix64 bits (core.random seeds 31 / 32), Strassen-Winograd with the
+device default cutoff over the default base-case engine (tcgen05
+kind::mxf4; `--engine` selects another). N = 1: one GPU multiplies. N > 1
+(torchrun): C and A row-sharded, B broadcast from rank 0 over NVLink (NCCL)
+in K-panels inside the timed step.
 
 `--impl reference` times the reference algorithm's CPU port
 (oracle/libgf2oracle.so, a C restatement of gf2mat's M4RM + Strassen-
