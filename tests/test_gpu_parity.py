@@ -327,6 +327,11 @@ def test_cfg5_addmul_digest(digests):
     c0 = g.random(n, n, 53)
     g.addmul(c0, a, b)
     assert O.digest(c0.to_numpy()) == digests["cfg5_addmul"]
+    # depth 1 with 32768^3 leaves: the tensor-core leaf launch splits K into
+    # 8192-entry chunks while fusing the post-addition into C (red.xor)
+    c0 = g.random(n, n, 53)
+    g.addmul(c0, a, b, g.MulParams(cutoff=32768, k=8))
+    assert O.digest(c0.to_numpy()) == digests["cfg5_addmul"]
 
 
 def test_freivalds_detects_fault():
