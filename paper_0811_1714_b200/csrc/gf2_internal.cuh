@@ -134,6 +134,8 @@ struct UmmaJob {
     cudaEvent_t b_ready;  // if set: B's source is produced on another stream
 };
 int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s);
+int launch_umma_f4(const UmmaJob &jb, int64_t nprob, cudaStream_t s);  // gf2_umma_f4.cu
+int num_sms();
 // multiply engine for every product (gf2_set_engine): 0 M4RM, 1 tcgen05 i8, 2 tcgen05 f8, 3 tcgen05 mxf4
 extern int g_engine;
 // Products below ~1e10 bit-ops run faster on the M4RM kernel than through

@@ -308,8 +308,6 @@ int launch_rpt(const KArgs &ka, const CUtensorMap &ta, const CUtensorMap &tb, in
     return check_cuda(cudaGetLastError(), "k_m4rm launch");
 }
 
-int g_num_sms = 0;
-
 // kernel timer (gf2_timer_*): event pairs around each M4RM launch
 struct TimedLaunch {
     cudaEvent_t a, b;
@@ -372,12 +370,6 @@ void timer_end(int idx, cudaStream_t s) {
 int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     if (!b.m || !b.n || !b.nprob) return GF2_OK;
     const int64_t Wn = words_per_row(b.n), Wl = words_per_row(b.l);
-    if (!g_num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
-    }
     auto zero_c = [&]() -> int {
         if (b.nprob == 1 || b.sc == b.m * b.pc) {
             gf2_view v{b.C, b.pc, b.m * b.nprob, b.n};
@@ -392,7 +384,7 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     if (b.l == 0) return b.accumulate ? GF2_OK : zero_c();
 
     const int64_t col_tiles = (Wn + kTileWords - 1) / kTileWords;
-    const int64_t want = g_num_sms;  // one CTA per SM is resident (smem-bound)
+    const int64_t want = num_sms();  // one CTA per SM is resident (smem-bound)
     int rpt = 16;
     int64_t row_tiles = (b.m + kRowGroups * rpt - 1) / (kRowGroups * rpt);
     while (rpt > 4 && row_tiles * col_tiles * b.nprob < want) {

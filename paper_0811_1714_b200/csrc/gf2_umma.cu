@@ -26,141 +26,11 @@
 #include <algorithm>
 #include <vector>
 
-#include "gf2_internal.cuh"
+#include "gf2_tc.cuh"
 
 namespace gf2 {
 
 namespace {
-
-constexpr int BM = 128, BN = 256, BK = 128;
-constexpr int UMMA_THREADS = 256;
-constexpr int64_t F8_KCHUNK = 8192;
-
-// ------------------------------------------------------------------ PTX
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2,
-                                            uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-        "[%5];\n" ::"r"(dst),
-        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
-        : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
-
-// UMMA shared-memory descriptor (sm_100 "version 1"), 128-byte swizzle.
-__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-    d |= 1ull << 46;  // version
-    d |= 2ull << 61;  // SWIZZLE_128B
-    return d;
-}
-
-template <int KIND>  // 0: kind::i8 (u8 x u8 -> s32), 1: kind::f8f6f4 (e4m3 -> f32)
-__device__ __forceinline__ void umma(uint32_t taddr, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
-    if (KIND == 0)
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(taddr),
-            "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
-    else
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(taddr),
-            "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ bool elect_one() {
-    uint32_t pred = 0;
-    asm volatile(
-        "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\n@P mov.s32 %0, 1;\n}\n"
-        : "+r"(pred));
-    return pred != 0;
-}
-
-
-#define TMEM_LD32(taddr, r)                                                                                    \
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"  \
-                 "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"              \
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),        \
-                   "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),    \
-                   "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), \
-                   "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), \
-                   "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                          \
-                 : "r"(taddr))
-
-#define TMEM_LD16(taddr, r)                                                                                    \
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, " \
-                 "[%16];\n"                                                                                     \
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),        \
-                   "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),    \
-                   "=r"(r[14]), "=r"(r[15])                                                                    \
-                 : "r"(taddr))
-
-// ------------------------------------------------------------------ expand
-// bits -> bytes (0 or `one`), 64 entries per thread, batched over problems.
-// With fuse = 1 this is also the last Strassen level's pre-addition: output
-// problem q = 7p + i is the XOR of source problem p's quadrants in mask[i].
-struct ExpandArgs {
-    const u64 *src;
-    int64_t sp, sstride;
-    int64_t qoff[4];   // quadrant offsets, first fused level (2x leaf size when levels == 2)
-    int64_t qoff2[4];  // quadrant offsets, second fused level (leaf size)
-    unsigned mask[7];
-    int levels;        // fused Strassen levels: 0, 1 (q = 7p+i) or 2 (q = 49p+7i+j)
-    int64_t q0;        // first problem of this chunk (dst is indexed chunk-locally)
-    uint8_t *dst;
-    int64_t dp, dstride;
-    int64_t rows, cols;
-    uint32_t one;
-};
-
-// A warp expands 32 consecutive words (2 KiB of bytes): every lane loads one
-// word, then the 128 16-byte chunks are written lane-contiguously (512 B per
-// store instruction) with the source word fetched by shuffle. LEVELS = fused
-// Strassen levels (0, 1, 2): up to 1, 4 or 16 source blocks XORed per word,
-// all gathers issued before use; two rows per iteration for more MLP.
-template <int LEVELS>
-__device__ __forceinline__ u64 gather_word(const ExpandArgs &a, const u64 *s, int64_t r, unsigned m1,
-                                           unsigned m2) {
-    u64 x = 0;
-    if (LEVELS == 0) {
-        x = __ldg(s + r * a.sp);
-    } else if (LEVELS == 1) {
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-            if (m1 & (1u << t)) x ^= __ldg(s + a.qoff[t] + r * a.sp);
-    } else {
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-            if ((m1 >> (k >> 2)) & (m2 >> (k & 3)) & 1u) x ^= __ldg(s + a.qoff[k >> 2] + a.qoff2[k & 3] + r * a.sp);
-    }
-    return x;
-}
 
 __device__ __forceinline__ void expand_store(const ExpandArgs &a, uint8_t *drow, u64 x, int lane, int64_t nbytes) {
 #pragma unroll
@@ -203,81 +73,6 @@ __global__ void k_expand(ExpandArgs a) {
         expand_store(a, d + r * a.dp, x0, lane, nbytes);
         if (r2 < a.rows) expand_store(a, d + r2 * a.dp, x1, lane, nbytes);
     }
-}
-
-// ------------------------------------------------------------------ gemm
-struct UArgs {
-    u64 *C;
-    int64_t pc, sc;
-    int64_t m, n, Wn;
-    int mt, nt, kblocks, kchunk_blocks, nchunks;
-    int64_t nprob;
-    int mode;  // 0 store, 1 xor, 2 atomic xor
-    // last Strassen level's post-addition fused into the epilogue: product
-    // q = 7p + i is XORed (red.global.xor) into the quadrants post_mask[i] of
-    // the level-(d-1) product p at C + p*sc + qoffC[Q] (C pre-zeroed).
-    int64_t q0;  // global index of this launch's problem 0 (C addressing)
-    int post;
-    int64_t qoffC[4];
-    unsigned post_mask[7];
-};
-
-template <int CG>
-__device__ __forceinline__ void umma_commit_cg(uint32_t bar) {
-    if (CG == 1)
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
-                     : "memory");
-    else
-        asm volatile(
-            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
-                bar),
-            "h"((uint16_t)3)
-            : "memory");
-}
-
-template <int KIND, int CG>
-__device__ __forceinline__ void umma_cg(uint32_t taddr, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
-    if (CG == 1) {
-        umma<KIND>(taddr, ad, bd, idesc, acc);
-    } else if (KIND == 0) {
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(taddr),
-            "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
-    } else {
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(taddr),
-            "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
-    }
-}
-
-// 2-SM TMA: each CTA loads its half into its own smem; the transaction bytes
-// land on the leader CTA's barrier (peer bit cleared).
-__device__ __forceinline__ void tma_load_3d_2sm(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2,
-                                                uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-        "%3, %4}], [%5];\n" ::"r"(dst),
-        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar & 0xFEFFFFFFu)
-        : "memory");
-}
-
-__device__ __forceinline__ void cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-    return r;
-}
-
-// arrive on the leader CTA's copy of a barrier (cluster scope)
-__device__ __forceinline__ void mbar_arrive_leader(uint32_t bar) {
-    uint32_t remote;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(remote) : "r"(bar));
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote) : "memory");
 }
 
 __device__ __forceinline__ void store_row(const UArgs &p, const uint32_t *packed, int64_t row, int ntile,
@@ -838,421 +633,6 @@ __global__ void __launch_bounds__(CV_THREADS, 1) k_umma_cv(CvArgs cv, UArgs p) {
     }
 }
 
-// ------------------------------------------------------------------ FP4 (kind::mxf4)
-// Entries as e2m1 nibbles (1.0 = 0x2, two per byte), both operands K-major,
-// block-scaled MMA with every scale = 1.0 (UE8M0 0x7F): twice the 8-bit MMA
-// rate and half the operand bytes. f32 accumulators, K chunks <= 8192 as for
-// kind::f8f6f4. K order inside every 64-entry group is permuted identically
-// on both sides (a fixed relabelling of the summation index): a 64-bit
-// K-vector v (bit i = entry i) becomes 8 words, word t holding nibbles
-// v[t], v[32+t], v[8+t], v[40+t], v[16+t], v[48+t], v[24+t], v[56+t].
-constexpr int F4_BN = 224;                 // max tile N (7 x 32-bit output groups)
-constexpr int F4_BNH = F4_BN / 2;          // B rows per CTA of a pair
-constexpr int F4_STG = 7;
-constexpr int F4_A_ST = BM * BK;           // 128 rows x 128 B (256 K entries)
-constexpr int F4_B_ST = F4_BNH * BK;       // 112 rows x 128 B
-constexpr int F4_SMEM = F4_STG * (F4_A_ST + F4_B_ST) + 2048;
-constexpr int F4_SF_COL = 2 * F4_BN;       // TMEM columns 448..511: constant scale factors
-constexpr int64_t F4_KCHUNK = 8192;
-static_assert(F4_SMEM <= 232448, "k_umma_f4 shared memory");
-
-// word t of a K-vector's 32 nibble bytes (see the permutation above)
-__device__ __forceinline__ uint32_t nib_word(u64 v, int t) {
-    const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
-    return (((lo >> t) & 0x01010101u) << 1) | (((hi >> t) & 0x01010101u) << 5);
-}
-
-// A side: a warp expands 32 consecutive words of 4 rows; every store
-// instruction writes 512 contiguous bytes (lane l: 16-byte chunk l + 32k of
-// the warp's 1 KiB, i.e. half l & 1 of word l/2 + 16k, fetched by shuffle).
-constexpr int F4_ROWS_PER_WARP = 4;
-template <int LEVELS>
-__global__ void __launch_bounds__(256) k_expand4_rows(ExpandArgs a) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t width = words_per_row(a.cols);
-    const int64_t j0 = (int64_t)blockIdx.x * 32, j = j0 + lane;
-    const int64_t r0 = ((int64_t)blockIdx.y * 8 + warp) * F4_ROWS_PER_WARP;
-    if (r0 >= a.rows) return;
-    const u64 tm = (j == width - 1) ? tail_mask(a.cols) : ~0ULL;
-    const int64_t q = a.q0 + blockIdx.z;
-    const int64_t p = LEVELS == 0 ? q : (LEVELS == 1 ? q / 7 : q / 49);
-    const unsigned m1 = LEVELS == 0 ? 1u : a.mask[LEVELS == 1 ? q % 7 : (q / 7) % 7];
-    const unsigned m2 = LEVELS == 2 ? a.mask[q % 7] : 1u;
-    const u64 *s = a.src + p * a.sstride + j;
-    u64 x[F4_ROWS_PER_WARP];
-#pragma unroll
-    for (int rr = 0; rr < F4_ROWS_PER_WARP; ++rr)
-        x[rr] = (j < width && r0 + rr < a.rows) ? __brevll(gather_word<LEVELS>(a, s, r0 + rr, m1, m2) & tm) : 0;
-    uint8_t *d = a.dst + (int64_t)blockIdx.z * a.dstride + j0 * 32;
-    const int h = lane & 1;
-#pragma unroll
-    for (int rr = 0; rr < F4_ROWS_PER_WARP; ++rr) {
-        if (r0 + rr >= a.rows) break;
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int wl = (lane >> 1) + 16 * k;
-            const u64 v = __shfl_sync(0xffffffffu, x[rr], wl);
-            if (j0 + wl < width)
-                *reinterpret_cast<uint4 *>(d + (r0 + rr) * a.dp + (lane + 32 * k) * 16) =
-                    make_uint4(nib_word(v, 4 * h), nib_word(v, 4 * h + 1), nib_word(v, 4 * h + 2),
-                               nib_word(v, 4 * h + 3));
-        }
-    }
-}
-
-// Fused level, all 7 outputs of one source problem at once: a warp loads the
-// 4 quadrant words of 32 consecutive words x 4 rows ONCE, forms the 7
-// combinations (mask[i]) and writes each one's nibbles like k_expand4_rows
-// (output problem 7p + i). Quadrant words are read once instead of 14
-// times per 7 outputs.
-template <int ROWS>
-__global__ void __launch_bounds__(256) k_expand4_rows7(ExpandArgs a) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t width = words_per_row(a.cols);
-    const int64_t j0 = (int64_t)blockIdx.x * 32, j = j0 + lane;
-    const int64_t r0 = ((int64_t)blockIdx.y * 8 + warp) * ROWS;
-    if (r0 >= a.rows) return;
-    const u64 tm = (j == width - 1) ? tail_mask(a.cols) : ~0ULL;
-    const int64_t p = a.q0 / 7 + blockIdx.z;  // source problem
-    const u64 *s = a.src + p * a.sstride + j;
-    const bool live = j < width;
-    u64 qw[ROWS][4];
-#pragma unroll
-    for (int rr = 0; rr < ROWS; ++rr)
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-            qw[rr][t] = (live && r0 + rr < a.rows) ? __ldg(s + a.qoff[t] + (r0 + rr) * a.sp) & tm : 0;
-    const int h = lane & 1;
-#pragma unroll 1
-    for (int i = 0; i < 7; ++i) {
-        const unsigned m = a.mask[i];
-        uint8_t *d = a.dst + ((int64_t)blockIdx.z * 7 + i) * a.dstride + j0 * 32;
-#pragma unroll
-        for (int rr = 0; rr < ROWS; ++rr) {
-            if (r0 + rr >= a.rows) break;
-            u64 x = 0;
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-                if (m & (1u << t)) x ^= qw[rr][t];
-            x = __brevll(x);
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                const int wl = (lane >> 1) + 16 * k;
-                const u64 v = __shfl_sync(0xffffffffu, x, wl);
-                if (j0 + wl < width)
-                    *reinterpret_cast<uint4 *>(d + (r0 + rr) * a.dp + (lane + 32 * k) * 16) =
-                        make_uint4(nib_word(v, 4 * h), nib_word(v, 4 * h + 1), nib_word(v, 4 * h + 2),
-                                   nib_word(v, 4 * h + 3));
-            }
-        }
-    }
-}
-
-// B side, transposed. A block stages 256 K rows x 16 words (coalesced 128 B
-// row segments, fused quadrant XORs) in shared memory; each warp then owns
-// 2 words: per 64-row K block, four warp-wide 32 x 32 transposes turn the
-// 64 x 64 bit block into 64 column K-vectors (lane: columns lane and lane + 32), and each lane writes
-// its two columns' 128 contiguous bytes (256 K entries).
-constexpr int F4T_ROWS = 256, F4T_WORDS = 16;
-constexpr int F4T_STG_PITCH = 144;  // 128 B output row + 16 B pad (conflict-free)
-constexpr int F4T_TILE_BYTES = F4T_ROWS * (F4T_WORDS + 1) * 8;
-constexpr int F4T_SMEM = F4T_TILE_BYTES + 8 * 32 * F4T_STG_PITCH;
-template <int LEVELS>
-__global__ void __launch_bounds__(256) k_expand4_cols(ExpandArgs a) {
-    extern __shared__ __align__(16) unsigned char f4t_smem[];
-    u64(*tile)[F4T_WORDS + 1] = reinterpret_cast<u64(*)[F4T_WORDS + 1]>(f4t_smem);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t width = words_per_row(a.cols);
-    const int64_t w0 = (int64_t)blockIdx.x * F4T_WORDS;
-    const int64_t k0 = (int64_t)blockIdx.y * F4T_ROWS;
-    const int64_t q = a.q0 + blockIdx.z;
-    const int64_t p = LEVELS == 0 ? q : (LEVELS == 1 ? q / 7 : q / 49);
-    const unsigned m1 = LEVELS == 0 ? 1u : a.mask[LEVELS == 1 ? q % 7 : (q / 7) % 7];
-    const unsigned m2 = LEVELS == 2 ? a.mask[q % 7] : 1u;
-    const u64 *s = a.src + p * a.sstride;
-#pragma unroll 4
-    for (int i = 0; i < F4T_ROWS * F4T_WORDS / 256; ++i) {
-        const int idx = threadIdx.x + 256 * i;
-        const int rr = idx / F4T_WORDS, ww = idx % F4T_WORDS;
-        const int64_t r = k0 + rr, w = w0 + ww;
-        u64 x = 0;
-        if (r < a.rows && w < width) {
-            x = gather_word<LEVELS>(a, s + w, r, m1, m2);
-            if (w == width - 1) x &= tail_mask(a.cols);
-        }
-        tile[rr][ww] = x;
-    }
-    __syncthreads();
-    const int64_t kbytes = a.dp;  // bytes per output row
-#pragma unroll 1
-    for (int u = 0; u < F4T_WORDS / 8; ++u) {
-        const int ww = warp * (F4T_WORDS / 8) + u;
-        const int64_t w = w0 + ww;
-        if (w >= width) break;
-        u64 ca[4], cb[4];  // column lane / lane + 32, K block kb (64 entries each)
-#pragma unroll
-        for (int kb = 0; kb < 4; ++kb) {
-            const u64 x0 = tile[kb * 64 + lane][ww], x1 = tile[kb * 64 + 32 + lane][ww];
-            const uint32_t c0a = transpose32(__brev((uint32_t)(x0 >> 32)), lane);
-            const uint32_t c0b = transpose32(__brev((uint32_t)(x1 >> 32)), lane);
-            const uint32_t c1a = transpose32(__brev((uint32_t)x0), lane);
-            const uint32_t c1b = transpose32(__brev((uint32_t)x1), lane);
-            ca[kb] = ((u64)c0b << 32) | c0a;
-            cb[kb] = ((u64)c1b << 32) | c1a;
-        }
-        // stage this word's 64 output rows (128 B each) in shared memory, then
-        // write them with coalesced 512-byte warp stores (8 lanes per row)
-        const int64_t nbytes = kbytes - k0 / 2 < 128 ? kbytes - k0 / 2 : 128;
-        uint8_t *d = a.dst + (int64_t)blockIdx.z * a.dstride + (w * 64) * a.dp + k0 / 2;
-        uint8_t *stg = f4t_smem + F4T_TILE_BYTES + warp * 32 * F4T_STG_PITCH;
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-#pragma unroll
-            for (int kb = 0; kb < 4; ++kb) {
-                const u64 v = half ? cb[kb] : ca[kb];
-                uint4 *o = reinterpret_cast<uint4 *>(stg + lane * F4T_STG_PITCH + 32 * kb);
-                o[0] = make_uint4(nib_word(v, 0), nib_word(v, 1), nib_word(v, 2), nib_word(v, 3));
-                o[1] = make_uint4(nib_word(v, 4), nib_word(v, 5), nib_word(v, 6), nib_word(v, 7));
-            }
-            __syncwarp();
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int row = 4 * i + (lane >> 3), off = (lane & 7) * 16;
-                if (off < nbytes)
-                    *reinterpret_cast<uint4 *>(d + (int64_t)(half * 32 + row) * a.dp + off) =
-                        *reinterpret_cast<const uint4 *>(stg + row * F4T_STG_PITCH + off);
-            }
-            __syncwarp();
-        }
-    }
-}
-
-__device__ __forceinline__ void umma_f4(uint32_t taddr, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc,
-                                        uint32_t sfa, uint32_t sfb) {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}\n" ::"r"(taddr),
-        "l"(ad), "l"(bd), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb));
-}
-
-// 32-bit group g of a row (columns 32g..32g+31, MSB-first) is u32 index g^1
-// of the row's little-endian 64-bit words.
-__device__ __forceinline__ void store_row_f4(const UArgs &p, const uint32_t *packed, int64_t row, int64_t g0,
-                                             int nch, int64_t gprob) {
-    if (row >= p.m) return;
-    uint32_t v[F4_BN / 32];
-    uint32_t keep[F4_BN / 32];
-#pragma unroll
-    for (int c = 0; c < F4_BN / 32; ++c) {
-        const int64_t rem = p.n - (g0 + c) * 32;
-        v[c] = (c < nch && rem > 0) ? packed[c] : 0u;
-        keep[c] = (c < nch && rem > 0 && rem < 32) ? (~0u >> rem) : 0u;
-        if (keep[c]) v[c] &= ~keep[c];
-    }
-    if (p.post) {
-        const unsigned dm = p.post_mask[gprob % 7];
-        const u64 *cbase = p.C + (gprob / 7) * p.sc + row * p.pc;
-#pragma unroll
-        for (int Q = 0; Q < 4; ++Q) {
-            if (!(dm & (1u << Q))) continue;
-            unsigned *crow = reinterpret_cast<unsigned *>(const_cast<u64 *>(cbase + p.qoffC[Q]));
-#pragma unroll
-            for (int c = 0; c < F4_BN / 32; ++c)
-                if (v[c]) atomicXor(crow + ((g0 + c) ^ 1), v[c]);
-        }
-        return;
-    }
-    unsigned *crow = reinterpret_cast<unsigned *>(p.C + gprob * p.sc + row * p.pc);
-#pragma unroll
-    for (int c = 0; c < F4_BN / 32; ++c) {
-        if (c >= nch || (g0 + c) * 32 >= p.n) break;
-        unsigned *w = crow + ((g0 + c) ^ 1);
-        if (p.mode == 2) {
-            if (v[c]) atomicXor(w, v[c]);
-        } else if (p.mode == 1) {
-            *w ^= v[c];
-        } else {
-            *w = keep[c] ? ((*w & keep[c]) | v[c]) : v[c];
-        }
-    }
-}
-
-// Persistent CTA-pair kernel (cluster of 2, tcgen05.mma.cta_group::2), tiles
-// 256 x (32..224), 128 B = 256 K entries per stage. TMEM: accumulators at columns 0 and 224, scale factors
-// (all 0x7F) at 448..511 in both CTAs.
-__global__ void __launch_bounds__(UMMA_THREADS, 1)
-    k_umma_f4(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, UArgs p) {
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
-    const uint32_t sA = base_u32;
-    const uint32_t sB = base_u32 + F4_STG * F4_A_ST;
-    const uint32_t sBar = sB + F4_STG * F4_B_ST;
-    const uint32_t bar_full = sBar, bar_empty = sBar + 8 * F4_STG, bar_tfull = sBar + 16 * F4_STG,
-                   bar_tempty = bar_tfull + 16;
-    const uint32_t tmem_holder = bar_tempty + 16;
-    unsigned char *gen_base = smem_raw + (base_u32 - smem_u32(smem_raw));
-    volatile uint32_t *tmem_holder_ptr = reinterpret_cast<volatile uint32_t *>(gen_base + (tmem_holder - base_u32));
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();
-    const int64_t unit = blockIdx.x >> 1, nunits = gridDim.x >> 1;
-    if (warp == 0 && lane == 0) {
-        for (int s = 0; s < F4_STG; ++s) {
-            mbar_init(bar_full + 8 * s, 1);
-            mbar_init(bar_empty + 8 * s, 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(bar_tfull + 8 * b, 1);
-            mbar_init(bar_tempty + 8 * b, 256);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
-        asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
-    }
-    if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(tmem_holder)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
-    }
-    tc_fence_before();
-    cluster_sync();
-    tc_fence_after();
-    const uint32_t tmem_base = *tmem_holder_ptr;
-    if (warp >= 4) {  // scale factors: every byte of columns 448..511 = 2^0
-        const uint32_t one = 0x7F7F7F7Fu;
-        const uint32_t ta = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + F4_SF_COL;
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-            asm volatile(
-                "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
-                "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(ta + 32 * h),
-                "r"(one)
-                : "memory");
-        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-    }
-    tc_fence_before();
-    cluster_sync();
-    tc_fence_after();
-
-    const int64_t tiles_per_chunk = p.nprob * p.mt * p.nt;
-    const int64_t ntiles = tiles_per_chunk * p.nchunks;
-    // column tiles: the row's 32-column groups spread evenly over p.nt tiles
-    // of <= 7 groups (4096 columns: 14 x 224 + 5 x 192), so no tile is a
-    // narrow, TMA-bound remainder; starts stay 32-bit-word aligned
-    const int ngroups = (int)((p.n + 31) / 32);
-    const int gq = ngroups / p.nt, gr = ngroups % p.nt;
-    auto tile_g0 = [&](int ntile) -> int { return ntile * gq + min(ntile, gr); };
-    auto tile_width = [&](int ntile) -> int { return 32 * (gq + (ntile < gr ? 1 : 0)); };
-
-    if (warp == 0 && lane == 0) {
-        int stage = 0;
-        uint32_t phase = 0;
-        for (int64_t t = unit; t < ntiles; t += nunits) {
-            const int chunk = (int)(t / tiles_per_chunk);
-            int64_t r = t % tiles_per_chunk;
-            const int prob = (int)(r / (p.mt * p.nt));
-            r %= (p.mt * p.nt);
-            const int mtile = (int)(r / p.nt), ntile = (int)(r % p.nt);
-            const int kb0 = chunk * p.kchunk_blocks;
-            const int kb1 = min(kb0 + p.kchunk_blocks, p.kblocks);
-            const int arow = mtile * 256 + (int)rank * BM;
-            const int brow = 32 * tile_g0(ntile) + (int)rank * (tile_width(ntile) / 2);
-            for (int kb = kb0; kb < kb1; ++kb) {
-                const uint32_t fb = bar_full + 8 * stage;
-                mbar_wait(bar_empty + 8 * stage, phase ^ 1);
-                if (rank == 0) mbar_expect_tx(fb, 2 * (F4_A_ST + F4_B_ST));
-                tma_load_3d_2sm(sA + stage * F4_A_ST, &tmA, kb * BK, arow, prob, fb);
-                tma_load_3d_2sm(sB + stage * F4_B_ST, &tmB, kb * BK, brow, prob, fb);
-                if (++stage == F4_STG) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-            }
-        }
-    } else if (warp == 1 && rank == 0) {
-        // The whole warp walks the pipeline (warp-uniform control flow, so the
-        // descriptors stay in uniform registers); one elected lane issues.
-        // block-scaled idesc: a/b format E2M1 (1) at bits 7/10, K-major both,
-        // N >> 3 at 17, scale format UE8M0 at 23, M >> 4 at 24, scale ids 0
-        const uint32_t idesc0 = (1u << 7) | (1u << 10) | (1u << 23) | ((uint32_t)(256 >> 4) << 24);
-        const uint32_t sfa = tmem_base + F4_SF_COL, sfb = tmem_base + F4_SF_COL + 32;
-        const uint64_t adesc0 = smem_desc(sA, 16, 1024), bdesc0 = smem_desc(sB, 16, 1024);
-        int stage = 0;
-        uint32_t phase = 0;
-        int it = 0;
-        for (int64_t t = unit; t < ntiles; t += nunits, ++it) {
-            const int chunk = (int)(t / tiles_per_chunk);
-            const int ntile = (int)((t % tiles_per_chunk) % p.nt);
-            const uint32_t idesc = idesc0 | ((uint32_t)(tile_width(ntile) >> 3) << 17);
-            const int kb0 = chunk * p.kchunk_blocks;
-            const int kb1 = min(kb0 + p.kchunk_blocks, p.kblocks);
-            const int acc = it & 1;
-            const uint32_t acc_phase = (it >> 1) & 1;
-            mbar_wait(bar_tempty + 8 * acc, acc_phase ^ 1);
-            tc_fence_after();
-            const uint32_t taddr = tmem_base + acc * F4_BN;
-            for (int kb = kb0; kb < kb1; ++kb) {
-                mbar_wait(bar_full + 8 * stage, phase);
-                tc_fence_after();
-                if (elect_one()) {
-                    const uint64_t ad = adesc0 + (uint64_t)((stage * F4_A_ST) >> 4);
-                    const uint64_t bd = bdesc0 + (uint64_t)((stage * F4_B_ST) >> 4);
-#pragma unroll
-                    for (int k = 0; k < BK / 32; ++k)
-                        umma_f4(taddr, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u, sfa, sfb);
-                    umma_commit_cg<2>(bar_empty + 8 * stage);
-                }
-                __syncwarp();
-                if (++stage == F4_STG) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-            }
-            if (elect_one()) umma_commit_cg<2>(bar_tfull + 8 * acc);
-            __syncwarp();
-        }
-    } else if (warp >= 4) {
-        const int q = warp & 3;
-        int it = 0;
-        for (int64_t t = unit; t < ntiles; t += nunits, ++it) {
-            int64_t r = t % tiles_per_chunk;
-            const int prob = (int)(r / (p.mt * p.nt));
-            r %= (p.mt * p.nt);
-            const int mtile = (int)(r / p.nt), ntile = (int)(r % p.nt);
-            const int nch = tile_width(ntile) >> 5;
-            const int acc = it & 1;
-            const uint32_t acc_phase = (it >> 1) & 1;
-            mbar_wait(bar_tfull + 8 * acc, acc_phase);
-            tc_fence_after();
-            uint32_t packed[F4_BN / 32];
-#pragma unroll
-            for (int c = 0; c < F4_BN / 32; ++c) {
-                packed[c] = 0;
-                if (c < nch) {
-                    uint32_t v[32];
-                    TMEM_LD32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * F4_BN + c * 32, v);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                    uint32_t pk = 0;
-#pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        pk = (pk << 1) | (__float_as_uint(__uint_as_float(v[j]) + 8388608.0f) & 1u);
-                    packed[c] = pk;
-                }
-            }
-            tc_fence_before();
-            mbar_arrive_leader(bar_tempty + 8 * acc);
-            const int64_t row = (int64_t)mtile * 256 + (int64_t)rank * BM + q * 32 + lane;
-            store_row_f4(p, packed, row, (int64_t)tile_g0(ntile), nch, p.q0 + prob);
-        }
-    }
-    tc_fence_before();
-    cluster_sync();
-    if (warp == 2) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem_base) : "memory");
-    }
-}
-
 // ------------------------------------------------------------------ host
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
@@ -1270,24 +650,19 @@ int get_encode() {
     return GF2_OK;
 }
 
-// 3-D byte tensor (inner, outer, problems) with a 128 x 128 box, 128-byte swizzle.
-int make_map(CUtensorMap *map, void *base, uint64_t inner, uint64_t outer, uint64_t nprob, uint64_t pitch,
-             uint64_t pstride, uint32_t box_outer = 128) {
-    GF2_TRY(get_encode());
-    cuuint64_t dims[3] = {inner, outer, nprob};
-    cuuint64_t strides[2] = {pitch, pstride};
-    cuuint32_t box[3] = {128, box_outer, 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return set_error(GF2_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-    return GF2_OK;
-}
-
 int g_sms = 0;
 
 }  // namespace
+
+int num_sms() {
+    if (!g_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_sms <= 0) g_sms = 148;
+    }
+    return g_sms;
+}
 
 int encode_map_3d(CUtensorMap *map, CUtensorMapDataType dt, void *base, const uint64_t dims[3],
                   const uint64_t strides[2], const uint32_t box[3], bool swizzle128) {
@@ -1319,151 +694,6 @@ int launch_expand(const ExpandArgs &a, int64_t nprob, cudaStream_t s) {
     return check_cuda(cudaGetLastError(), "k_expand launch");
 }
 
-int launch_expand4(const ExpandArgs &a, int64_t nprob, bool cols, cudaStream_t s) {
-    const int64_t width = words_per_row(a.cols);
-    if (!a.rows || !width || !nprob) return GF2_OK;
-    if (!cols && a.levels == 1 && a.q0 % 7 == 0 && nprob % 7 == 0) {
-        dim3 grd((unsigned)((width + 31) / 32), (unsigned)((a.rows + 8 * 4 - 1) / (8 * 4)), (unsigned)(nprob / 7));
-        k_expand4_rows7<4><<<grd, 256, 0, s>>>(a);
-        note_launch();
-        return check_cuda(cudaGetLastError(), "k_expand4_rows7 launch");
-    }
-    if (!cols) {
-        dim3 grd((unsigned)((width + 31) / 32), (unsigned)((a.rows + 8 * F4_ROWS_PER_WARP - 1) / (8 * F4_ROWS_PER_WARP)),
-                 (unsigned)nprob);
-        if (a.levels == 0)
-            k_expand4_rows<0><<<grd, 256, 0, s>>>(a);
-        else if (a.levels == 1)
-            k_expand4_rows<1><<<grd, 256, 0, s>>>(a);
-        else
-            k_expand4_rows<2><<<grd, 256, 0, s>>>(a);
-    } else {
-        // a.dp = bytes per K-major row = (K rows rounded to 64) / 2
-        dim3 grd((unsigned)((width + F4T_WORDS - 1) / F4T_WORDS), (unsigned)((a.dp * 2 + F4T_ROWS - 1) / F4T_ROWS),
-                 (unsigned)nprob);
-        static bool attr = false;
-        if (!attr) {
-            GF2_TRY(check_cuda(cudaFuncSetAttribute(k_expand4_cols<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    F4T_SMEM), "expand4 smem attr"));
-            GF2_TRY(check_cuda(cudaFuncSetAttribute(k_expand4_cols<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    F4T_SMEM), "expand4 smem attr"));
-            GF2_TRY(check_cuda(cudaFuncSetAttribute(k_expand4_cols<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    F4T_SMEM), "expand4 smem attr"));
-            attr = true;
-        }
-        if (a.levels == 0)
-            k_expand4_cols<0><<<grd, 256, F4T_SMEM, s>>>(a);
-        else if (a.levels == 1)
-            k_expand4_cols<1><<<grd, 256, F4T_SMEM, s>>>(a);
-        else
-            k_expand4_cols<2><<<grd, 256, F4T_SMEM, s>>>(a);
-    }
-    note_launch();
-    return check_cuda(cudaGetLastError(), "k_expand4 launch");
-}
-
-// FP4 engine (kind::mxf4, CTA pairs): A as nibble rows (m x kb bytes), B
-// transposed to nibble rows (n x kb bytes), kb = round64(l) / 2.
-int launch_umma_f4(const UmmaJob &jb, int64_t nprob, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma_f4, cudaFuncAttributeMaxDynamicSharedMemorySize, F4_SMEM),
-                           "umma_f4 smem attr"));
-        attr = true;
-    }
-    const int64_t kb = (jb.l + 63) / 64 * 32;   // bytes per nibble row
-    const int64_t np = (jb.n + 63) / 64 * 64;   // B rows (columns of B), whole words
-    const int64_t per = jb.m * kb + np * kb;
-    const int64_t cap = (int64_t)8 << 30;
-    int64_t qchunk = std::max<int64_t>(1, std::min<int64_t>(nprob, cap / std::max<int64_t>(per, 1)));
-    if (jb.fuse_pre == 1 && qchunk >= 7) qchunk -= qchunk % 7;  // whole 7-product groups (k_expand4_rows7)
-    uint8_t *ws = nullptr;
-    GF2_TRY(pool_setup());
-    cudaError_t e = cudaMallocAsync((void **)&ws, (size_t)(qchunk * per), s);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        return set_error(GF2_ERR_OOM, std::string("umma workspace: ") + cudaGetErrorString(e));
-    }
-    uint8_t *a4 = ws, *b4 = ws + qchunk * jb.m * kb;
-    const int64_t f2 = jb.fuse_pre == 2 ? 2 : 1;
-    ExpandArgs ea{};
-    ea.src = jb.A; ea.sp = jb.pa; ea.sstride = jb.sa; ea.levels = jb.fuse_pre;
-    ea.qoff[1] = f2 * jb.l / 64; ea.qoff[2] = f2 * jb.m * jb.pa; ea.qoff[3] = ea.qoff[1] + ea.qoff[2];
-    ea.qoff2[1] = jb.l / 64; ea.qoff2[2] = jb.m * jb.pa; ea.qoff2[3] = ea.qoff2[1] + ea.qoff2[2];
-    for (int i = 0; i < 7; ++i) ea.mask[i] = jb.maskA[i];
-    ea.dst = a4; ea.dp = kb; ea.dstride = jb.m * kb; ea.rows = jb.m; ea.cols = jb.l;
-    // B side: row expansion of B^T when given transposed, else the
-    // transposing column expansion of B
-    const bool bt = jb.b_trans != 0;
-    const int64_t brows = bt ? jb.n : jb.l, bcols = bt ? jb.l : jb.n;
-    ExpandArgs eb{};
-    eb.src = jb.B; eb.sp = jb.pb; eb.sstride = jb.sb; eb.levels = jb.fuse_pre;
-    eb.qoff[1] = f2 * bcols / 64; eb.qoff[2] = f2 * brows * jb.pb; eb.qoff[3] = eb.qoff[1] + eb.qoff[2];
-    eb.qoff2[1] = bcols / 64; eb.qoff2[2] = brows * jb.pb; eb.qoff2[3] = eb.qoff2[1] + eb.qoff2[2];
-    for (int i = 0; i < 7; ++i) eb.mask[i] = jb.maskB[i];
-    eb.dst = b4; eb.dp = kb; eb.dstride = np * kb; eb.rows = brows; eb.cols = bcols;
-
-    UArgs ua{};
-    ua.C = jb.C; ua.pc = jb.pc; ua.sc = jb.sc;
-    ua.m = jb.m; ua.n = jb.n; ua.Wn = words_per_row(jb.n);
-    ua.mt = (int)((jb.m + 255) / 256);
-    // GF2_F4_BN: maximum column-tile width (tuning knob; 224 measured best)
-    static const int f4bn = getenv("GF2_F4_BN") ? std::max(32, std::min(F4_BN, atoi(getenv("GF2_F4_BN")))) : F4_BN;
-    ua.nt = (int)((jb.n + f4bn - 1) / f4bn);
-    ua.kblocks = (int)((kb + BK - 1) / BK);
-    ua.kchunk_blocks = (int)(F4_KCHUNK / (2 * BK));
-    ua.nchunks = (ua.kblocks + ua.kchunk_blocks - 1) / ua.kchunk_blocks;
-    ua.post = jb.fuse_post;
-    int rc = GF2_OK;
-    if (jb.fuse_post) {
-        ua.qoffC[1] = jb.n / 64; ua.qoffC[2] = jb.m * jb.pc; ua.qoffC[3] = ua.qoffC[1] + ua.qoffC[2];
-        for (int i = 0; i < 7; ++i) ua.post_mask[i] = jb.maskC[i];
-        ua.mode = 2;
-    } else if (ua.nchunks > 1) {
-        if (!jb.accumulate)
-            for (int64_t q = 0; q < nprob && rc == GF2_OK; ++q) {
-                gf2_view v{jb.C + q * jb.sc, jb.pc, jb.m, jb.n};
-                rc = launch_zero(v, s);
-            }
-        ua.mode = 2;
-    } else {
-        ua.mode = jb.accumulate ? 1 : 0;
-    }
-    for (int64_t q0 = 0; q0 < nprob && rc == GF2_OK; q0 += qchunk) {
-        const int64_t nq = std::min<int64_t>(qchunk, nprob - q0);
-        ea.q0 = eb.q0 = ua.q0 = q0;
-        ua.nprob = nq;
-        rc = launch_expand4(ea, nq, false, s);
-        if (rc == GF2_OK && jb.b_ready && q0 == 0) rc = check_cuda(cudaStreamWaitEvent(s, jb.b_ready, 0), "join wait");
-        if (rc == GF2_OK) rc = launch_expand4(eb, nq, !bt, s);
-        CUtensorMap ta, tb;
-        if (rc == GF2_OK) rc = make_map(&ta, a4, (uint64_t)kb, (uint64_t)jb.m, (uint64_t)nq, kb, jb.m * kb);
-        if (rc == GF2_OK)  // rows past n (never written on the B^T path) read as zeros
-            rc = make_map(&tb, b4, (uint64_t)kb, (uint64_t)jb.n, (uint64_t)nq, kb, np * kb, F4_BNH);
-        if (rc != GF2_OK) break;
-        const int64_t ntiles = (int64_t)ua.nchunks * nq * ua.mt * ua.nt;
-        const int64_t pairs = std::min<int64_t>(ntiles, g_sms / 2);
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3((unsigned)(2 * pairs));
-        cfg.blockDim = dim3(UMMA_THREADS);
-        cfg.dynamicSmemBytes = F4_SMEM;
-        cfg.stream = s;
-        cudaLaunchAttribute la[1];
-        la[0].id = cudaLaunchAttributeClusterDimension;
-        la[0].val.clusterDim.x = 2;
-        la[0].val.clusterDim.y = 1;
-        la[0].val.clusterDim.z = 1;
-        cfg.attrs = la;
-        cfg.numAttrs = 1;
-        const int tidx = timer_begin(s, (double)jb.m * (double)jb.l * (double)jb.n * (double)nq);
-        rc = check_cuda(cudaLaunchKernelEx(&cfg, k_umma_f4, ta, tb, ua), "k_umma_f4 launch");
-        note_launch();
-        timer_end(tidx, s);
-    }
-    cudaFreeAsync(ws, s);
-    return rc;
-}
-
 // The tensor-core product for a batch: C (^)= A.B per problem, byte expansion
 // (optionally fused with the last Strassen pre-addition) + tcgen05 GEMM
 // (optionally fused with the last post-addition). kind: 0 i8, 1 f8, 2 f4.
@@ -1479,10 +709,8 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
         }
         return GF2_OK;
     }
-    if (!g_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    static bool umma_attr = false;  // the 8-bit kernels' shared-memory opt-in, once
+    if (!umma_attr) {
         GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 Geo<1>::SMEM), "umma smem attr"));
         GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1491,6 +719,7 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
                                                 Geo<2>::SMEM), "umma smem attr"));
         GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 Geo<2>::SMEM), "umma smem attr"));
+        umma_attr = true;
     }
     if (kind == 2) return launch_umma_f4(jb, nprob, s);
     // i8 with 2-SM pairs: operand tiles built in shared memory from the packed
@@ -1536,7 +765,7 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
             ua.mode = jb.accumulate ? 1 : 0;
         }
         const int64_t tiles = nprob * ua.mt * ua.nt;
-        const int64_t pairs = std::min<int64_t>(tiles, g_sms / 2);
+        const int64_t pairs = std::min<int64_t>(tiles, num_sms() / 2);
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)(2 * pairs));
         cfg.blockDim = dim3(CV_THREADS);
@@ -1633,13 +862,13 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
         const int64_t ntiles = (int64_t)ua.nchunks * nq * ua.mt * ua.nt;
         const int tidx = timer_begin(s, (double)jb.m * (double)jb.l * (double)jb.n * (double)nq);
         if (cg == 1) {
-            const int grid = (int)(ntiles < g_sms ? ntiles : g_sms);
+            const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
             if (kind == 0)
                 k_umma<0, 1><<<grid, UMMA_THREADS, Geo<1>::SMEM, s>>>(ta, tb, ua);
             else
                 k_umma<1, 1><<<grid, UMMA_THREADS, Geo<1>::SMEM, s>>>(ta, tb, ua);
         } else {
-            const int64_t pairs = std::min<int64_t>(ntiles, g_sms / 2);
+            const int64_t pairs = std::min<int64_t>(ntiles, num_sms() / 2);
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3((unsigned)(2 * pairs));
             cfg.blockDim = dim3(UMMA_THREADS);
