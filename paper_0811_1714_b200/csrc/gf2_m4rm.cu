@@ -30,6 +30,7 @@
 // rows of B to 128 columns (1024 bit-ops / 16 B = 64 bit-ops per byte);
 // table builds add 2^8/BM of that traffic. The kernel is bound by the
 // 128 B/clk/SM shared-memory crossbar.
+#include <algorithm>
 #include <vector>
 
 #include "gf2_internal.cuh"
@@ -369,6 +370,20 @@ void timer_end(int idx, cudaStream_t s) {
 
 int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     if (!b.m || !b.n || !b.nprob) return GF2_OK;
+    // gridDim.z = K splits (<= 8) x problems must stay <= 65535: deep
+    // recursions (7^6 leaves at cutoff 64) run their leaves in chunks
+    constexpr int64_t kMaxBatch = 65535 / 8;
+    if (b.nprob > kMaxBatch) {
+        for (int64_t q0 = 0; q0 < b.nprob; q0 += kMaxBatch) {
+            M4rmBatch c = b;
+            c.A += q0 * b.sa;
+            c.B += q0 * b.sb;
+            c.C += q0 * b.sc;
+            c.nprob = std::min<int64_t>(kMaxBatch, b.nprob - q0);
+            GF2_TRY(launch_m4rm(c, s));
+        }
+        return GF2_OK;
+    }
     const int64_t Wn = words_per_row(b.n), Wl = words_per_row(b.l);
     auto zero_c = [&]() -> int {
         if (b.nprob == 1 || b.sc == b.m * b.pc) {

@@ -225,9 +225,13 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
 int strassen_core(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0, int depth, int accumulate,
                   cudaStream_t s) {
     if (g_engine != 0) {
-        double leaf = (double)(A0.nrows >> depth) * (double)(A0.ncols >> depth) * (double)(B0.ncols >> depth);
+        // tensor-core leaves when the batch is big enough to amortize the
+        // expansion and each leaf is at least one 256-row x 256-column tile
+        const int64_t lm = A0.nrows >> depth, ll = A0.ncols >> depth, ln = B0.ncols >> depth;
+        double leaf = (double)lm * (double)ll * (double)ln;
         for (int i = 0; i < depth; ++i) leaf *= 7.0;
-        if (leaf >= tensor_min_work()) return strassen_core_tc(C0, A0, B0, depth, accumulate, s);
+        if (leaf >= tensor_min_work() && lm >= 256 && ln >= 256 && ll >= 256)
+            return strassen_core_tc(C0, A0, B0, depth, accumulate, s);
     }
     int64_t M[24], L[24], N[24], Lw[24], Nw[24], P[24];
     for (int i = 0; i <= depth; ++i) {

@@ -698,9 +698,23 @@ int launch_expand(const ExpandArgs &a, int64_t nprob, cudaStream_t s) {
 // (optionally fused with the last Strassen pre-addition) + tcgen05 GEMM
 // (optionally fused with the last post-addition). kind: 0 i8, 1 f8, 2 f4.
 int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
-    const int64_t nprob = jb.nsrc * (jb.fuse_pre == 2 ? 49 : (jb.fuse_pre == 1 ? 7 : 1));
+    const int64_t per_src = jb.fuse_pre == 2 ? 49 : (jb.fuse_pre == 1 ? 7 : 1);
+    const int64_t nprob = jb.nsrc * per_src;
     if (!jb.m || !jb.n || !nprob) return GF2_OK;
-    if (nprob > 65535) return set_error(GF2_ERR_PARAMETER, "too many problems for the tensor-core path");
+    // the expansion grids index problems in gridDim.z (<= 65535): larger
+    // batches run in chunks of source problems (C problems follow sources)
+    const int64_t max_src = 65535 / per_src;
+    if (jb.nsrc > max_src) {
+        for (int64_t s0 = 0; s0 < jb.nsrc; s0 += max_src) {
+            UmmaJob c = jb;
+            c.A += s0 * jb.sa;
+            c.B += s0 * jb.sb;
+            c.C += s0 * jb.sc;
+            c.nsrc = std::min<int64_t>(max_src, jb.nsrc - s0);
+            GF2_TRY(launch_umma_job(c, kind, s));
+        }
+        return GF2_OK;
+    }
     if (jb.l == 0) {
         if (jb.accumulate || jb.fuse_post) return GF2_OK;
         for (int64_t q = 0; q < nprob; ++q) {

@@ -229,3 +229,25 @@ def test_two_fused_levels_option(engine, digests):
                          capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     assert out.stdout.strip().splitlines()[-1] == digests["cfg3"]
+
+
+@pytest.mark.parametrize("engine", ["m4rm", "tc-f4"])
+def test_deep_recursion_many_leaves(engine):
+    """Fuzzer regression: cutoff 64 on 4546x12000x12000 recurses to depth 6
+    (7^6 = 117649 leaves), more problems than one launch's gridDim.z holds;
+    leaves run in chunks (tiny leaves go to M4RM on every engine)."""
+    g.set_engine(engine)
+    m, l, n = 4546, 12000, 12000
+    want = P.mul_strassen(O.random(m, l, 3), O.random(l, n, 4), cutoff=64).words
+    got = g.mul_strassen(g.random(m, l, 3), g.random(l, n, 4), g.MulParams(cutoff=64, k=8))
+    assert np.array_equal(words(got), want)
+
+
+@pytest.mark.parametrize("engine", ["tc-f4", "tc-i8"])
+def test_cfg3_depth6_tensor_leaves_chunked(engine, digests):
+    """cfg3 at cutoff 256: depth 6, 117649 tensor-core leaves of 256^3 --
+    the tensor job runs in chunks of source problems."""
+    g.set_engine(engine)
+    a, b = g.random(16384, 16384, 31), g.random(16384, 16384, 32)
+    c = g.mul_strassen(a, b, g.MulParams(cutoff=256, k=8))
+    assert O.digest(words(c)) == digests["cfg3"]
