@@ -3,7 +3,10 @@ offsets x cutoffs, every result compared bit-exactly with the C port of the
 reference algorithm (itself pinned to the reference's golden vectors by
 tests/test_oracle.py). Runs for a time budget; writes a JSON summary.
 
-    python tools/fuzz.py SECONDS [OUT.json]
+    python tools/fuzz.py SECONDS [OUT.json] [--big]
+
+--big: tensor engines only, shapes 512..9000, cutoffs 512..4096, so the
+recursions run with tensor-core leaves (fewer, larger cases).
 """
 import json, sys, time, traceback
 import numpy as np
@@ -15,14 +18,20 @@ from oracle import gf2_port as P
 
 torch.cuda.set_device(0)
 P.set_threads(P.max_threads())
-budget = float(sys.argv[1]) if len(sys.argv) > 1 else 600
-out = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/fuzz.json"
+args = [x for x in sys.argv[1:] if not x.startswith("--")]
+BIG = "--big" in sys.argv
+budget = float(args[0]) if args else 600
+out = args[1] if len(args) > 1 else "gpurun_out/fuzz.json"
 rng = np.random.default_rng(int(time.time()))
-ENGINES = ["m4rm", "tc-i8", "tc-f8", "tc-f4"]
+ENGINES = ["tc-i8", "tc-f8", "tc-f4"] if BIG else ["m4rm", "tc-i8", "tc-f8", "tc-f4"]
 OPS = ["mul_m4rm", "mul_direct", "mul_strassen", "addmul", "addmul_direct", "mul_m4rm_into"]
 
 
 def dim(big):
+    if BIG:
+        if rng.random() < 0.4:
+            return max(512, 256 * int(rng.integers(2, 36)) + int(rng.integers(-2, 3)))
+        return int(rng.integers(512, 9001))
     r = rng.random()
     hi = 6000 if big else 1500
     if r < 0.15:
@@ -61,7 +70,7 @@ while time.time() < t_end:
         ha = host_window(pa.to_numpy(), ra, ca, m, l)
         hb = host_window(pb.to_numpy(), rb, cb, l, nn)
         want = P.mul_strassen(ha, hb, cutoff=64).words
-        cutoff = int(rng.choice([64, 128, 256, 512, 1024, 2048]))
+        cutoff = int(rng.choice([512, 1024, 2048, 4096] if BIG else [64, 128, 256, 512, 1024, 2048]))
         case.update(window=win, cutoff=cutoff)
         if op in ("mul_m4rm", "mul_direct", "mul_strassen"):
             if op == "mul_m4rm":
