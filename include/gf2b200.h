@@ -52,6 +52,12 @@ enum {
 const char *gf2_version(void);
 const char *gf2_last_error(void);
 
+/* Workspace (Strassen level buffers, tensor-core operands) comes from the
+ * device's stream-ordered pool, which keeps freed memory cached between
+ * calls (cfg5 peaks near 16 GB). This synchronizes the current device and
+ * returns the cached memory to the system. */
+int gf2_release_workspace(void);
+
 /* Wait for all work queued on `stream` (NULL: the whole device). The
  * library links the CUDA runtime statically, so hosts that do not use CUDA
  * themselves synchronize through this call. */

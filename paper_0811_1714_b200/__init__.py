@@ -9,7 +9,7 @@ the library or the GPU is missing, operations raise NativeUnavailable.
 """
 
 from ._lib import (DeviceError, NativeUnavailable, get_engine, launch_count,
-                   set_engine)
+                   release_workspace, set_engine)
 from .core import (BitMatrix, HostMatrix, MatrixWindow, add, add_into,
                    bernoulli, copy_into, copy_out, create, equal,
                    first_difference, from_dense, from_host, from_numpy,
@@ -36,7 +36,8 @@ __all__ = [
     "from_dense", "from_host", "from_numpy", "get_engine", "identity",
     "launch_count",
     "mul_direct", "mul_m4rm", "mul_m4rm_blocked", "mul_m4rm_into", "mul_m4rm_multitable",
-    "mul_strassen", "peel_split", "random", "set_engine", "tail_mask",
+    "mul_strassen", "peel_split", "random", "release_workspace", "set_engine",
+    "tail_mask",
     "to_dense",
     "to_numpy", "trailing_bits_clean", "window", "words_per_row", "zero_into",
     "augment", "load", "mul_cubic", "save", "stack", "transpose",

@@ -65,6 +65,7 @@ SIGNATURES = {
                        + [ctypes.POINTER(ctypes.c_int64)]),
     "gf2_launch_count": (ctypes.c_int64, []),
     "gf2_timer_enable": (ctypes.c_int, [ctypes.c_int]),
+    "gf2_release_workspace": (ctypes.c_int, []),
     "gf2_stream_sync": (ctypes.c_int, [ctypes.c_void_p]),
     "gf2_set_engine": (ctypes.c_int, [ctypes.c_int]),
     "gf2_get_engine": (ctypes.c_int, []),
@@ -159,6 +160,13 @@ def set_engine(name: str) -> None:
     if name not in ENGINES:
         raise ValueError(f"engine {name!r} not in {sorted(ENGINES)}")
     check(load().gf2_set_engine(ENGINES[name]))
+
+
+def release_workspace() -> None:
+    """Return the device workspace cached by the stream-ordered pool
+    (Strassen level buffers, tensor-core operands) to the system;
+    synchronizes the current device."""
+    check(lib_cuda().gf2_release_workspace())
 
 
 def get_engine() -> str:

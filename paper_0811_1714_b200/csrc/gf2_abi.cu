@@ -88,6 +88,15 @@ const char *gf2_version(void) { return "gf2b200 0.1.0 (sm_100a)"; }
 
 const char *gf2_last_error(void) { return t_err.c_str(); }
 
+int gf2_release_workspace(void) {
+    int dev = 0;
+    GF2_TRY(check_cuda(cudaGetDevice(&dev), "cudaGetDevice"));
+    GF2_TRY(check_cuda(cudaDeviceSynchronize(), "cudaDeviceSynchronize"));
+    cudaMemPool_t pool;
+    GF2_TRY(check_cuda(cudaDeviceGetDefaultMemPool(&pool, dev), "cudaDeviceGetDefaultMemPool"));
+    return check_cuda(cudaMemPoolTrimTo(pool, 0), "cudaMemPoolTrimTo");
+}
+
 int gf2_stream_sync(void *stream) {
     if (!stream) return check_cuda(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
     return check_cuda(cudaStreamSynchronize((cudaStream_t)stream), "cudaStreamSynchronize");

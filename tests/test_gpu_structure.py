@@ -119,3 +119,17 @@ def test_to_host_returns_reference_matrix_when_gf2mat_is_imported(monkeypatch):
     assert isinstance(hw, StubBitMatrix) and np.array_equal(hw.words, w.to_numpy())
     monkeypatch.delitem(sys.modules, "gf2mat")
     assert isinstance(a.to_host(), g.HostMatrix)
+
+
+def test_release_workspace_returns_pool_memory():
+    """gf2_release_workspace: the stream-ordered pool's cached workspace goes
+    back to the system and later products still run."""
+    import torch
+    a, b = g.random(8192, 8192, 1), g.random(8192, 8192, 2)
+    c = g.mul_strassen(a, b, g.MulParams(cutoff=4096))
+    torch.cuda.synchronize()
+    before = torch.cuda.mem_get_info()[0]
+    g.release_workspace()
+    after = torch.cuda.mem_get_info()[0]
+    assert after >= before
+    assert g.equal(g.mul_strassen(a, b, g.MulParams(cutoff=4096)), c)
