@@ -122,6 +122,19 @@ int gf2_mul(const gf2_view *c, const gf2_view *a, const gf2_view *b,
 int gf2_strassen(const gf2_view *c, const gf2_view *a, const gf2_view *b,
                  int64_t cutoff, int k, int accumulate, void *stream);
 
+/* Multiply plans (CUDA graphs): capture one gf2_strassen call on fixed
+ * views -- its recursion, workspace allocation, side-stream fork/join and
+ * every launch -- into a graph, then replay it with a single launch. The
+ * views' device buffers must outlive the plan; each launch reads their
+ * current contents (accumulate = 1 adds A.B to C's current contents). This
+ * removes the per-call host work (validation, planning, tensor-map encoding,
+ * 4-6 launches, ~45 us) from loops that multiply the same shapes. */
+typedef struct gf2_plan gf2_plan;
+int gf2_plan_strassen(gf2_plan **out, const gf2_view *c, const gf2_view *a, const gf2_view *b, int64_t cutoff,
+                      int k, int accumulate);
+int gf2_plan_launch(gf2_plan *plan, void *stream);
+int gf2_plan_destroy(gf2_plan *plan);
+
 /* core.py:374-376 `transpose`: out (a.ncols x a.nrows) = a^T (bit-matrix
  * transpose, 64x64 blocks per warp). */
 int gf2_transpose(const gf2_view *out, const gf2_view *a, void *stream);

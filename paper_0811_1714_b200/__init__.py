@@ -20,8 +20,8 @@ from .errors import (AlignmentError, DimensionError, FormatError, GF2MatError,
 from .m4rm import (StripeSpec, mul_m4rm, mul_m4rm_blocked, mul_m4rm_into,
                    mul_m4rm_multitable)
 from .gf2m import load, save
-from .strassen import (GPU_CUTOFF, MulParams, PeelSplit, addmul,
-                       addmul_direct, default_params, mul_direct,
+from .strassen import (GPU_CUTOFF, MulParams, PeelSplit, StrassenPlan,
+                       addmul, addmul_direct, default_params, mul_direct,
                        mul_strassen, peel_split)
 from .structure import augment, mul_cubic, stack, transpose
 
@@ -31,7 +31,7 @@ __all__ = [
     "AlignmentError", "BitMatrix", "DeviceError", "DimensionError",
     "FormatError", "GF2MatError", "GPU_CUTOFF", "HostMatrix", "MatrixWindow",
     "MulParams", "NativeUnavailable", "ParameterError", "PeelSplit",
-    "StripeSpec", "add", "add_into", "addmul", "addmul_direct", "bernoulli", "copy_into",
+    "StrassenPlan", "StripeSpec", "add", "add_into", "addmul", "addmul_direct", "bernoulli", "copy_into",
     "copy_out", "create", "default_params", "equal", "first_difference",
     "from_dense", "from_host", "from_numpy", "get_engine", "identity",
     "launch_count",

@@ -61,6 +61,10 @@ SIGNATURES = {
     "gf2_copy_cols": (ctypes.c_int, [_V, ctypes.c_int64, _V, _P]),
     "gf2_strassen": (ctypes.c_int, [_V, _V, _V, ctypes.c_int64, ctypes.c_int,
                                     ctypes.c_int, _P]),
+    "gf2_plan_strassen": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), _V, _V, _V,
+                                         ctypes.c_int64, ctypes.c_int, ctypes.c_int]),
+    "gf2_plan_launch": (ctypes.c_int, [_P, _P]),
+    "gf2_plan_destroy": (ctypes.c_int, [_P]),
     "gf2_peel_split": (ctypes.c_int, [ctypes.c_int64] * 4
                        + [ctypes.POINTER(ctypes.c_int64)]),
     "gf2_launch_count": (ctypes.c_int64, []),

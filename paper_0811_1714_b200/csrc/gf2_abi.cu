@@ -235,6 +235,58 @@ int gf2_strassen(const gf2_view *c, const gf2_view *a, const gf2_view *b, int64_
     return strassen_mul(*c, *a, *b, cutoff, accumulate ? 1 : 0, (cudaStream_t)stream);
 }
 
+struct gf2_plan {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+};
+
+int gf2_plan_strassen(gf2_plan **out, const gf2_view *c, const gf2_view *a, const gf2_view *b, int64_t cutoff,
+                      int k, int accumulate) {
+    if (!out) return set_error(GF2_ERR_PARAMETER, "null plan pointer");
+    *out = nullptr;
+    if (cutoff < 64) return set_error(GF2_ERR_PARAMETER, "cutoff " + std::to_string(cutoff) + " < 64");
+    if (k < 0 || k > 16) return set_error(GF2_ERR_PARAMETER, "k=" + std::to_string(k) + " outside 0..16");
+    GF2_TRY(check_mul(c, a, b));
+    GF2_TRY(pool_setup());
+    SideStream *sd = nullptr;
+    GF2_TRY(side_stream(&sd));  // created outside the capture
+    cudaStream_t cs = nullptr;
+    GF2_TRY(check_cuda(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "plan stream"));
+    // relaxed: the library's one-time lazy setup (function attributes,
+    // driver entry point) may run while capturing
+    int rc = check_cuda(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed), "begin capture");
+    cudaGraph_t graph = nullptr;
+    if (rc == GF2_OK) {
+        rc = strassen_mul(*c, *a, *b, cutoff, accumulate ? 1 : 0, cs);
+        const cudaError_t e = cudaStreamEndCapture(cs, &graph);
+        if (rc == GF2_OK) rc = check_cuda(e, "end capture");
+    }
+    cudaGraphExec_t exec = nullptr;
+    if (rc == GF2_OK) rc = check_cuda(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
+    cudaStreamDestroy(cs);
+    if (rc != GF2_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        return rc;
+    }
+    *out = new gf2_plan{graph, exec};
+    return GF2_OK;
+}
+
+int gf2_plan_launch(gf2_plan *plan, void *stream) {
+    if (!plan || !plan->exec) return set_error(GF2_ERR_PARAMETER, "null plan");
+    return check_cuda(cudaGraphLaunch(plan->exec, (cudaStream_t)stream), "graph launch");
+}
+
+int gf2_plan_destroy(gf2_plan *plan) {
+    if (!plan) return GF2_OK;
+    int rc = GF2_OK;
+    if (plan->exec) rc = check_cuda(cudaGraphExecDestroy(plan->exec), "graph exec destroy");
+    if (plan->graph) cudaGraphDestroy(plan->graph);
+    delete plan;
+    return rc;
+}
+
 int gf2_transpose(const gf2_view *out, const gf2_view *a, void *stream) {
     GF2_TRY(check_view(out, "out"));
     GF2_TRY(check_view(a, "a"));

@@ -131,3 +131,45 @@ def addmul_direct(c: Mat, a: Mat, b: Mat) -> None:
     _check_cuda_dev(c, a, b)
     _lib.check(_lib.lib_cuda().gf2_mul(c._view(), a._view(), b._view(), 1,
                                        _stream()))
+
+
+class StrassenPlan:
+    """A captured multiply (CUDA graph, gf2_plan_strassen): C (+)= A.B on
+    these matrices, replayed by `run()` with one graph launch instead of the
+    per-call host work of mul_strassen / addmul (~45 us: validation,
+    planning, tensor-map encoding, 4-6 launches). Each run reads the
+    operands' current contents, so a serving loop refills A and B in place
+    and re-runs. The plan keeps its matrices alive."""
+
+    def __init__(self, c: Mat, a: Mat, b: Mat, params: MulParams | None = None,
+                 accumulate: bool = False):
+        import ctypes
+        if a.ncols != b.nrows:
+            raise DimensionError(
+                f"inner dimensions {a.ncols} and {b.nrows} differ")
+        if c.nrows != a.nrows or c.ncols != b.ncols:
+            raise DimensionError(
+                f"target {c.nrows}x{c.ncols} != product {a.nrows}x{b.ncols}")
+        _check_cuda_dev(c, a, b)
+        params = params or default_params()
+        self._mats = (c, a, b)
+        self._lib = _lib.lib_cuda()
+        h = ctypes.c_void_p()
+        _lib.check(self._lib.gf2_plan_strassen(
+            ctypes.byref(h), c._view(), a._view(), b._view(),
+            int(params.cutoff), int(params.k), int(accumulate)))
+        self._h = h
+
+    @property
+    def c(self):
+        return self._mats[0]
+
+    def run(self) -> None:
+        """Launch the captured multiply on the current stream."""
+        _lib.check(self._lib.gf2_plan_launch(self._h, _stream()))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.gf2_plan_destroy(h)
+            self._h = None

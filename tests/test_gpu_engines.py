@@ -251,3 +251,29 @@ def test_cfg3_depth6_tensor_leaves_chunked(engine, digests):
     a, b = g.random(16384, 16384, 31), g.random(16384, 16384, 32)
     c = g.mul_strassen(a, b, g.MulParams(cutoff=256, k=8))
     assert O.digest(words(c)) == digests["cfg3"]
+
+
+@pytest.mark.parametrize("engine", ["tc-f4", "m4rm"])
+def test_strassen_plan_graph_replay(engine, digests):
+    """StrassenPlan (CUDA graph of one multiply): replays equal the eager
+    result, read the operands' current contents, and accumulate correctly."""
+    import torch
+    g.set_engine(engine)
+    n = 4096
+    a, b = g.random(n, n, 21), g.random(n, n, 22)
+    c = g.create(n, n)
+    plan = g.StrassenPlan(c, a, b, g.MulParams(cutoff=1024, k=8))
+    for _ in range(3):
+        plan.run()
+    torch.cuda.synchronize()
+    assert O.digest(words(c)) == digests["cfg2"]
+    g.copy_into(a, g.random(n, n, 99))          # refill in place, replay
+    plan.run()
+    assert g.equal(c, g.mul_strassen(a, b, g.MulParams(cutoff=1024, k=8)))
+    acc = g.random(n, n, 5)
+    acc0 = words(acc)
+    p2 = g.StrassenPlan(acc, a, b, g.MulParams(cutoff=2048), accumulate=True)
+    p2.run()
+    p2.run()                                    # C + AB + AB = C
+    assert np.array_equal(words(acc), acc0)
+    del plan, p2
