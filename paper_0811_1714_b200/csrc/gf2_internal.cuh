@@ -41,6 +41,18 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
     return x;
 }
 
+// Per-device one-time setup: function attributes (the dynamic shared-memory
+// opt-in) belong to the device context, so "done" is tracked per device.
+// Returns true the first time it is called for `flags` on the current device.
+inline bool first_on_device(bool (&flags)[64]) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return true;
+    if (flags[dev]) return false;
+    flags[dev] = true;
+    return true;
+}
+
 // Status plumbing ------------------------------------------------------
 int set_error(int code, const std::string &msg);
 int check_cuda(cudaError_t e, const char *what);

@@ -361,12 +361,10 @@ namespace gf2 {
 int launch_combine_t(const CombineArgs &a, cudaStream_t s) {
     if (!a.R || !a.W || !a.nprob) return GF2_OK;
     if (a.R % 64) return set_error(GF2_ERR_PARAMETER, "combine_t: rows not a multiple of 64");
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[64] = {};
+    if (first_on_device(attr))
         GF2_TRY(check_cuda(cudaFuncSetAttribute(k_combine_t, cudaFuncAttributeMaxDynamicSharedMemorySize, CT_SMEM),
                            "combine_t smem attr"));
-        attr = true;
-    }
     dim3 grd((unsigned)((a.W + CT_WORDS - 1) / CT_WORDS), (unsigned)((a.R + CT_ROWS - 1) / CT_ROWS), (unsigned)a.nprob);
     k_combine_t<<<grd, 256, CT_SMEM, s>>>(a);
     note_launch();

@@ -296,13 +296,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int RPT, bool TMA>
 int launch_rpt(const KArgs &ka, const CUtensorMap &ta, const CUtensorMap &tb, int64_t col_tiles, int64_t row_tiles,
                int64_t zdim, cudaStream_t s) {
-    static bool configured = false;
+    static bool configured[64] = {};
     constexpr int sm = smem_bytes<RPT>();
-    if (!configured) {
+    if (first_on_device(configured))
         GF2_TRY(check_cuda(cudaFuncSetAttribute(k_m4rm<RPT, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
                            "cudaFuncSetAttribute(k_m4rm)"));
-        configured = true;
-    }
     dim3 grid((unsigned)col_tiles, (unsigned)row_tiles, (unsigned)zdim);
     k_m4rm<RPT, TMA><<<grid, kThreads, sm, s>>>(ka, ta, tb);
     note_launch();

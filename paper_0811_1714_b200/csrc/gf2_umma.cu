@@ -723,8 +723,8 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
         }
         return GF2_OK;
     }
-    static bool umma_attr = false;  // the 8-bit kernels' shared-memory opt-in, once
-    if (!umma_attr) {
+    static bool umma_attr[64] = {};  // the 8-bit kernels' shared-memory opt-in, once per device
+    if (first_on_device(umma_attr)) {
         GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 Geo<1>::SMEM), "umma smem attr"));
         GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -733,7 +733,6 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
                                                 Geo<2>::SMEM), "umma smem attr"));
         GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 Geo<2>::SMEM), "umma smem attr"));
-        umma_attr = true;
     }
     if (kind == 2) return launch_umma_f4(jb, nprob, s);
     // i8 with 2-SM pairs: operand tiles built in shared memory from the packed
@@ -742,11 +741,10 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
     static const bool conv = getenv("GF2_UMMA_CONV") && atoi(getenv("GF2_UMMA_CONV")) == 1;
     static const int cgc = getenv("GF2_UMMA_CG") ? atoi(getenv("GF2_UMMA_CG")) : 2;
     if (kind == 0 && conv && cgc == 2 && jb.fuse_pre <= 1) {
-        static bool cv_attr = false;
-        if (!cv_attr) {
+        static bool cv_attr[64] = {};
+        if (first_on_device(cv_attr)) {
             GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma_cv, cudaFuncAttributeMaxDynamicSharedMemorySize, CV_SMEM),
                                "umma_cv smem attr"));
-            cv_attr = true;
         }
         CvArgs cv{};
         cv.A = jb.A; cv.pa = jb.pa; cv.sa = jb.sa;

@@ -452,15 +452,14 @@ static int launch_expand4(const ExpandArgs &a, int64_t nprob, bool cols, cudaStr
         // a.dp = bytes per K-major row = (K rows rounded to 64) / 2
         dim3 grd((unsigned)((width + F4T_WORDS - 1) / F4T_WORDS), (unsigned)((a.dp * 2 + F4T_ROWS - 1) / F4T_ROWS),
                  (unsigned)nprob);
-        static bool attr = false;
-        if (!attr) {
+        static bool attr[64] = {};
+        if (first_on_device(attr)) {
             GF2_TRY(check_cuda(cudaFuncSetAttribute(k_expand4_cols<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     F4T_SMEM), "expand4 smem attr"));
             GF2_TRY(check_cuda(cudaFuncSetAttribute(k_expand4_cols<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     F4T_SMEM), "expand4 smem attr"));
             GF2_TRY(check_cuda(cudaFuncSetAttribute(k_expand4_cols<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     F4T_SMEM), "expand4 smem attr"));
-            attr = true;
         }
         if (a.levels == 0)
             k_expand4_cols<0><<<grd, 256, F4T_SMEM, s>>>(a);
@@ -476,11 +475,10 @@ static int launch_expand4(const ExpandArgs &a, int64_t nprob, bool cols, cudaStr
 // FP4 engine (kind::mxf4, CTA pairs): A as nibble rows (m x kb bytes), B
 // transposed to nibble rows (n x kb bytes), kb = round64(l) / 2.
 int launch_umma_f4(const UmmaJob &jb, int64_t nprob, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[64] = {};
+    if (first_on_device(attr)) {
         GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma_f4, cudaFuncAttributeMaxDynamicSharedMemorySize, F4_SMEM),
                            "umma_f4 smem attr"));
-        attr = true;
     }
     const int64_t kb = (jb.l + 63) / 64 * 32;   // bytes per nibble row
     const int64_t np = (jb.n + 63) / 64 * 64;   // B rows (columns of B), whole words
