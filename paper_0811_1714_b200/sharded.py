@@ -21,15 +21,21 @@ _WORD = 64
 
 
 def shard_rows(m: int, world: int, rank: int, align: int = _WORD):
-    """Row range [r0, r1) of rank `rank`: equal blocks rounded up to
-    `align` rows (so Strassen quadrants stay aligned), last rank short."""
+    """Row range [r0, r1) of rank `rank`: the `align`-row blocks (so Strassen
+    quadrants stay aligned) dealt out as evenly as possible, the first ranks
+    taking one extra block; with fewer than `align` rows per rank, a plain
+    balanced split."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError(f"rank {rank} outside world {world}")
-    per = -(-m // world)
-    per = -(-per // align) * align if m >= align * world else per
-    r0 = min(m, rank * per)
-    r1 = min(m, r0 + per)
-    return r0, r1
+    if m < align * world:
+        per, extra = divmod(m, world)
+        r0 = rank * per + min(rank, extra)
+        return r0, r0 + per + (1 if rank < extra else 0)
+    blocks = -(-m // align)
+    per, extra = divmod(blocks, world)
+    b0 = rank * per + min(rank, extra)
+    b1 = b0 + per + (1 if rank < extra else 0)
+    return min(m, b0 * align), min(m, b1 * align)
 
 
 def k_panels(l: int, npanels: int) -> list[tuple[int, int]]:
