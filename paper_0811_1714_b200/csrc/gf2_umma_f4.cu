@@ -224,17 +224,37 @@ __device__ __forceinline__ void store_row_f4(const UArgs &p, const uint32_t *pac
         keep[c] = (c < nch && rem > 0 && rem < 32) ? (~0u >> rem) : 0u;
         if (keep[c]) v[c] &= ~keep[c];
     }
+    // XOR-accumulate into a row: adjacent groups (2w, 2w+1) share the
+    // 64-bit word w (group 2w in its high half), so they go out as one
+    // red.xor.b64 -- 4 atomics per row instead of 7. The start group's
+    // parity is warp-uniform; both cases are unrolled so v[] stays in
+    // registers. A zero half contributed to a neighbour's word is a no-op.
+    auto red_row = [&](u64 *crow) {
+        if ((g0 & 1) == 0) {
+#pragma unroll
+            for (int c = 0; c < F4_BN / 32; c += 2) {
+                const u64 x = ((u64)v[c] << 32) | (c + 1 < F4_BN / 32 ? v[c + 1] : 0u);
+                if (x) atomicXor(reinterpret_cast<unsigned long long *>(crow + (g0 + c) / 2), (unsigned long long)x);
+            }
+        } else {
+            if (v[0]) atomicXor(reinterpret_cast<unsigned *>(crow) + (g0 ^ 1), v[0]);
+#pragma unroll
+            for (int c = 1; c < F4_BN / 32; c += 2) {
+                const u64 x = ((u64)v[c] << 32) | v[c + 1];
+                if (x) atomicXor(reinterpret_cast<unsigned long long *>(crow + (g0 + c) / 2), (unsigned long long)x);
+            }
+        }
+    };
     if (p.post) {
         const unsigned dm = p.post_mask[gprob % 7];
-        const u64 *cbase = p.C + (gprob / 7) * p.sc + row * p.pc;
+        u64 *cbase = p.C + (gprob / 7) * p.sc + row * p.pc;
 #pragma unroll
-        for (int Q = 0; Q < 4; ++Q) {
-            if (!(dm & (1u << Q))) continue;
-            unsigned *crow = reinterpret_cast<unsigned *>(const_cast<u64 *>(cbase + p.qoffC[Q]));
-#pragma unroll
-            for (int c = 0; c < F4_BN / 32; ++c)
-                if (v[c]) atomicXor(crow + ((g0 + c) ^ 1), v[c]);
-        }
+        for (int Q = 0; Q < 4; ++Q)
+            if (dm & (1u << Q)) red_row(cbase + p.qoffC[Q]);
+        return;
+    }
+    if (p.mode == 2) {
+        red_row(p.C + gprob * p.sc + row * p.pc);
         return;
     }
     unsigned *crow = reinterpret_cast<unsigned *>(p.C + gprob * p.sc + row * p.pc);
@@ -242,9 +262,7 @@ __device__ __forceinline__ void store_row_f4(const UArgs &p, const uint32_t *pac
     for (int c = 0; c < F4_BN / 32; ++c) {
         if (c >= nch || (g0 + c) * 32 >= p.n) break;
         unsigned *w = crow + ((g0 + c) ^ 1);
-        if (p.mode == 2) {
-            if (v[c]) atomicXor(w, v[c]);
-        } else if (p.mode == 1) {
+        if (p.mode == 1) {
             *w ^= v[c];
         } else {
             *w = keep[c] ? ((*w & keep[c]) | v[c]) : v[c];
