@@ -72,7 +72,8 @@ def peel_split(m: int, l: int, n: int, cutoff: int) -> PeelSplit:
 
 def default_params() -> MulParams:
     """Device defaults (the reference derives its from CPU cache sizes,
-    tuning.py:47-65): recursion above GPU_CUTOFF, M4RM below."""
+    tuning.py:47-65): recursion above GPU_CUTOFF, the selected base-case
+    engine below (tcgen05 kind::mxf4 by default; small leaves run M4RM)."""
     return MulParams(cutoff=GPU_CUTOFF, k=8, t=8)
 
 
@@ -85,7 +86,8 @@ def _strassen(c: Mat, a: Mat, b: Mat, params: MulParams,
 
 
 def mul_strassen(a: Mat, b: Mat, params: MulParams | None = None) -> BitMatrix:
-    """strassen.py:257-282 -- full dispatch: recursion, then M4RM."""
+    """strassen.py:257-282 -- full dispatch: peel, Strassen-Winograd
+    recursion, leaves on the base-case engine (set_engine), peel fix-ups."""
     if a.ncols != b.nrows:
         raise DimensionError(
             f"inner dimensions {a.ncols} and {b.nrows} differ")
