@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(256) k_expand4_rows(ExpandArgs a) {
 }
 
 // Fused level, all 7 outputs of one source problem at once: a warp loads the
-// 4 quadrant words of 32 consecutive words x 4 rows ONCE, forms the 7
+// 4 quadrant words of 32 consecutive words x ROWS rows ONCE, forms the 7
 // combinations (mask[i]) and writes each one's nibbles like k_expand4_rows
 // (output problem 7p + i). Quadrant words are read once instead of 14
 // times per 7 outputs.
@@ -452,8 +452,10 @@ static int launch_expand4(const ExpandArgs &a, int64_t nprob, bool cols, cudaStr
     const int64_t width = words_per_row(a.cols);
     if (!a.rows || !width || !nprob) return GF2_OK;
     if (!cols && a.levels == 1 && a.q0 % 7 == 0 && nprob % 7 == 0) {
-        dim3 grd((unsigned)((width + 31) / 32), (unsigned)((a.rows + 8 * 4 - 1) / (8 * 4)), (unsigned)(nprob / 7));
-        k_expand4_rows7<4><<<grd, 256, 0, s>>>(a);
+        // 2 rows per warp: 48 registers, more resident blocks and a finer grid
+        // than 4 (43 vs 45 us at cfg3; forcing occupancy via launch bounds spills)
+        dim3 grd((unsigned)((width + 31) / 32), (unsigned)((a.rows + 8 * 2 - 1) / (8 * 2)), (unsigned)(nprob / 7));
+        k_expand4_rows7<2><<<grd, 256, 0, s>>>(a);
         note_launch();
         return check_cuda(cudaGetLastError(), "k_expand4_rows7 launch");
     }
