@@ -45,7 +45,7 @@ def parse():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--cutoff", type=int, default=0,
                    help="Strassen cutoff (0 = device default)")
-    p.add_argument("--npanels", type=int, default=4)
+    p.add_argument("--npanels", type=int, default=2)
     p.add_argument("--engine", default="tc-f4", choices=["m4rm", "tc-i8", "tc-f8", "tc-f4"],
                    help="product engine (results are identical)")
     p.add_argument("--no-e2e", action="store_true")

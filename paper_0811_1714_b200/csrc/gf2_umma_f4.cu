@@ -253,7 +253,7 @@ __device__ __forceinline__ void store_row_f4(const UArgs &p, const uint32_t *pac
             if (dm & (1u << Q)) red_row(cbase + p.qoffC[Q]);
         return;
     }
-    if (p.mode == 2) {
+    if (p.mode >= 1) {  // XOR-accumulate (1) or K-chunk partials (2): fire-and-forget
         red_row(p.C + gprob * p.sc + row * p.pc);
         return;
     }
@@ -262,11 +262,7 @@ __device__ __forceinline__ void store_row_f4(const UArgs &p, const uint32_t *pac
     for (int c = 0; c < F4_BN / 32; ++c) {
         if (c >= nch || (g0 + c) * 32 >= p.n) break;
         unsigned *w = crow + ((g0 + c) ^ 1);
-        if (p.mode == 1) {
-            *w ^= v[c];
-        } else {
-            *w = keep[c] ? ((*w & keep[c]) | v[c]) : v[c];
-        }
+        *w = keep[c] ? ((*w & keep[c]) | v[c]) : v[c];
     }
 }
 

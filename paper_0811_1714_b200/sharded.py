@@ -68,7 +68,7 @@ def pipelined_broadcast(b_rows, panels: Sequence[tuple[int, int]],
 
 
 def mul_sharded(a_shard, b, params=None, src: int = 0, group=None,
-                npanels: int = 4, c=None):
+                npanels: int = 2, c=None):
     """C_p (+)= A_p . B on this rank. `b` is a BitMatrix of B's full shape
     on every rank; its contents matter only on `src`. If `c` is given the
     product is accumulated into it (addmul), else a fresh C_p is returned."""
