@@ -102,10 +102,8 @@ __device__ __forceinline__ void store_row(const UArgs &p, const uint32_t *packed
         const int64_t wi = (int64_t)ntile * (BN / 64) + w;
         if (wi >= p.Wn) break;
         const u64 v = ((u64)packed[2 * w] << 32) | (u64)packed[2 * w + 1];
-        if (p.mode == 2) {
+        if (p.mode >= 1) {  // XOR-accumulate / K-chunk partials: fire-and-forget red.xor, no epilogue load
             if (v) atomicXor(reinterpret_cast<unsigned long long *>(crow + wi), (unsigned long long)v);
-        } else if (p.mode == 1) {
-            crow[wi] ^= v;
         } else if (wi == p.Wn - 1 && ctm != ~0ULL) {
             crow[wi] = (crow[wi] & ~ctm) | v;
         } else {
