@@ -102,8 +102,10 @@ struct CombineArgs {
 // independent work that can overlap on the GPU (one user per call site at a
 // time: the host thread issues fork -> side work -> join in order).
 struct SideStream {
-    cudaStream_t s;
+    cudaStream_t s;              // default priority
     cudaEvent_t fork, join;
+    cudaStream_t hi;             // highest priority: work that should win SM slots
+    cudaEvent_t hi_fork, hi_join;
 };
 int side_stream(SideStream **out);
 int launch_combine(const CombineArgs &a, cudaStream_t s);

@@ -383,6 +383,11 @@ int side_stream(SideStream **out) {
         GF2_TRY(check_cuda(cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking), "side stream"));
         GF2_TRY(check_cuda(cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming), "fork event"));
         GF2_TRY(check_cuda(cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming), "join event"));
+        int least = 0, greatest = 0;
+        GF2_TRY(check_cuda(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range"));
+        GF2_TRY(check_cuda(cudaStreamCreateWithPriority(&sd.hi, cudaStreamNonBlocking, greatest), "hi stream"));
+        GF2_TRY(check_cuda(cudaEventCreateWithFlags(&sd.hi_fork, cudaEventDisableTiming), "fork event"));
+        GF2_TRY(check_cuda(cudaEventCreateWithFlags(&sd.hi_join, cudaEventDisableTiming), "join event"));
     }
     *out = &sd;
     return GF2_OK;
