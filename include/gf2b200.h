@@ -46,11 +46,24 @@ enum {
     GF2_ERR_PARAMETER = 3, /* ParameterError (errors.py:16) */
     GF2_ERR_CUDA = 4,      /* CUDA runtime failure (no reference analogue) */
     GF2_ERR_OOM = 5,       /* device allocation failure */
-    GF2_ERR_INTERNAL = 6
+    GF2_ERR_INTERNAL = 6,
+    GF2_ERR_NCCL = 7       /* NCCL missing or a collective failed */
 };
 
 const char *gf2_version(void);
 const char *gf2_last_error(void);
+
+/* row-sharded multi-GPU C_p (+)= A_p . B for hosts that
+ * run NCCL themselves (one process or thread per GPU). This rank passes its
+ * row shard of C and A and a device buffer `b` for all of B (its contents
+ * matter only on rank `src`); B is broadcast with ncclBroadcast in `npanels`
+ * word-aligned K-panels on an internal communication stream, and each panel
+ * is multiplied (Strassen-Winograd with `cutoff`) as soon as it has landed.
+ * `nccl_comm` is an ncclComm_t; NCCL is loaded at run time (libnccl.so.2).
+ * The Python package offers the same over torch.distributed
+ * (paper_0811_1714_b200.sharded.mul_sharded). */
+int gf2_mul_sharded(const gf2_view *c_shard, const gf2_view *a_shard, const gf2_view *b, void *nccl_comm,
+                    int src, int npanels, int64_t cutoff, int accumulate, void *stream);
 
 /* Workspace (Strassen level buffers, tensor-core operands) comes from the
  * device's stream-ordered pool, which keeps freed memory cached between

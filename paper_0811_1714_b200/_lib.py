@@ -22,6 +22,7 @@ GF2_ERR_PARAMETER = 3
 GF2_ERR_CUDA = 4
 GF2_ERR_OOM = 5
 GF2_ERR_INTERNAL = 6
+GF2_ERR_NCCL = 7
 
 
 class NativeUnavailable(RuntimeError):
@@ -69,6 +70,8 @@ SIGNATURES = {
                        + [ctypes.POINTER(ctypes.c_int64)]),
     "gf2_launch_count": (ctypes.c_int64, []),
     "gf2_timer_enable": (ctypes.c_int, [ctypes.c_int]),
+    "gf2_mul_sharded": (ctypes.c_int, [_V, _V, _V, _P, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int64, ctypes.c_int, _P]),
     "gf2_release_workspace": (ctypes.c_int, []),
     "gf2_stream_sync": (ctypes.c_int, [ctypes.c_void_p]),
     "gf2_set_engine": (ctypes.c_int, [ctypes.c_int]),

@@ -1,6 +1,7 @@
 // C-ABI entry points (include/gf2b200.h). Validation mirrors the checks and
 // messages of the reference functions each entry replaces, so the Python
 // shim raises the same exception classes for the same inputs.
+#include <nccl.h>
 #include <stdio.h>
 
 #include <string>
@@ -8,6 +9,8 @@
 #include "gf2_internal.cuh"
 
 namespace gf2 {
+int mul_sharded(const gf2_view &c, const gf2_view &a, const gf2_view &b, ncclComm_t comm, int src, int npanels,
+                int64_t cutoff, int accumulate, cudaStream_t s);
 int m4rm_mul(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accumulate, cudaStream_t s);
 int engine_mul(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accumulate, cudaStream_t s);
 int strassen_mul(const gf2_view &C, const gf2_view &A, const gf2_view &B, int64_t cutoff, int accumulate,
@@ -87,6 +90,16 @@ extern "C" {
 const char *gf2_version(void) { return "gf2b200 0.1.0 (sm_100a)"; }
 
 const char *gf2_last_error(void) { return t_err.c_str(); }
+
+int gf2_mul_sharded(const gf2_view *c_shard, const gf2_view *a_shard, const gf2_view *b, void *nccl_comm,
+                    int src, int npanels, int64_t cutoff, int accumulate, void *stream) {
+    if (!nccl_comm) return set_error(GF2_ERR_PARAMETER, "null NCCL communicator");
+    if (npanels < 1) return set_error(GF2_ERR_PARAMETER, "npanels " + std::to_string(npanels) + " < 1");
+    if (cutoff < 64) return set_error(GF2_ERR_PARAMETER, "cutoff " + std::to_string(cutoff) + " < 64");
+    GF2_TRY(check_mul(c_shard, a_shard, b));
+    return mul_sharded(*c_shard, *a_shard, *b, (ncclComm_t)nccl_comm, src, npanels, cutoff, accumulate ? 1 : 0,
+                       (cudaStream_t)stream);
+}
 
 int gf2_release_workspace(void) {
     int dev = 0;
