@@ -490,6 +490,12 @@ def main():
         "dtype": "u64", "data": "synthetic: core.random splitmix64 "
                                 f"Bernoulli(0.5) bits, seeds {w['seed_a']}/"
                                 f"{w['seed_b']}",
+        "compute": {"tc-f4": "GF(2) words as u64 (XOR additions); leaf products as "
+                             "e2m1 nibbles x e2m1 -> f32 (tcgen05 kind::mxf4, exact "
+                             "integer sums), parity of the f32 sum",
+                    "tc-i8": "u64 words; leaf products as u8 x u8 -> s32 (kind::i8), parity",
+                    "tc-f8": "u64 words; leaf products as e4m3 x e4m3 -> f32 (kind::f8f6f4), parity",
+                    "m4rm": "u64 words throughout (XOR of 128-bit Gray-table rows)"}[args.engine],
         "config": {"workload": f"{w['name']}: A,B {m}x{l} . {l}x{n} GF(2), "
                                f"Strassen-Winograd (cutoff {params.cutoff}) "
                                f"over the {args.engine} base case",
