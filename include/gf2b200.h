@@ -60,6 +60,9 @@ const char *gf2_last_error(void);
  * word-aligned K-panels on an internal communication stream, and each panel
  * is multiplied (Strassen-Winograd with `cutoff`) as soon as it has landed.
  * `nccl_comm` is an ncclComm_t; NCCL is loaded at run time (libnccl.so.2).
+ * Call it outside ncclGroupStart/End: the per-panel "landed" events are
+ * recorded right after each ncclBroadcast is issued, which a group would
+ * defer (a host thread driving several GPUs calls it once per device).
  * The Python package offers the same over torch.distributed
  * (paper_0811_1714_b200.sharded.mul_sharded). */
 int gf2_mul_sharded(const gf2_view *c_shard, const gf2_view *a_shard, const gf2_view *b, void *nccl_comm,
