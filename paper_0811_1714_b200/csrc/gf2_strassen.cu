@@ -109,7 +109,7 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
         if (rc == GF2_OK) rc = check_cuda(cudaStreamWaitEvent(sd->s, sd->fork, 0), "fork wait");
         if (rc == GF2_OK) rc = launch_transpose(Bt0, B0, sd->s);
         if (rc == GF2_OK) rc = check_cuda(cudaEventRecord(sd->join, sd->s), "join");
-        bt_ready = sd->join;
+        if (sd) bt_ready = sd->join;  // null when the side stream could not be created
     }
     for (int lv = 0; lv < lastA && rc == GF2_OK; ++lv) {
         for (int side = 0; side < 2 && rc == GF2_OK; ++side) {
