@@ -46,6 +46,9 @@ def parse():
     p.add_argument("--cutoff", type=int, default=0,
                    help="Strassen cutoff (0 = device default)")
     p.add_argument("--npanels", type=int, default=2)
+    p.add_argument("--sharded", action="store_true",
+                   help="run the multi-GPU (NCCL) step and e2e path even at "
+                        "N = 1 (a world of one; for testing it on one GPU)")
     p.add_argument("--engine", default="tc-f4", choices=["m4rm", "tc-i8", "tc-f8", "tc-f4"],
                    help="product engine (results are identical)")
     p.add_argument("--no-e2e", action="store_true")
@@ -252,6 +255,124 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ GPU arm
+def _free_port() -> int:
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def e2e_sharded(args, g, dev, stream, flush, a, r0, r1, w, params, world,
+                rank, c_dev):
+    """End to end at N ranks through the public API: every product, each
+    rank uploads its row shard of A and its block of B's rows (owned_rows)
+    from pinned host memory over its own PCIe link, mul_sharded(src=None)
+    broadcasts the blocks over NVLink while the panels multiply, and the
+    rank downloads its C shard. Returns (pipelined, serial): the pipelined
+    figure runs ShardedHostPipeline (copies of neighbouring products overlap
+    compute, as HostPipeline at N = 1), timed from the first upload to the
+    last download; both max over ranks; bytes are whole-job totals."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_0811_1714_b200.pipeline import ShardedHostPipeline
+    from paper_0811_1714_b200.sharded import mul_sharded, owned_rows
+
+    m, l, n = w["m"], w["l"], w["n"]
+    wa, wb = g.words_per_row(l), g.words_per_row(n)
+    mr = r1 - r0
+    ha = torch.empty((mr, wa), dtype=torch.int64, pin_memory=True)
+    hb = torch.empty((l, wb), dtype=torch.int64, pin_memory=True)
+    hcs = [torch.empty((mr, wb), dtype=torch.int64, pin_memory=True)
+           for _ in range(2)]
+    hav, hbv = ha.numpy().view(np.uint64), hb.numpy().view(np.uint64)
+    hcv = [x.numpy().view(np.uint64) for x in hcs]
+    a.to_numpy(out=hav)
+    mine = owned_rows(l, world, rank, None)
+    full_b = g.random(l, n, w["seed_b"], device=dev)
+    for k0, k1 in mine:
+        g.window(full_b, k0, 0, k1 - k0, n).to_numpy(out=hbv[k0:k1])
+    del full_b
+    want = c_dev.to_numpy()                   # this rank's digest-checked C
+    bitops = float(m) * l * n
+    h2d_rank = hav.nbytes + sum((k1 - k0) * wb * 8 for k0, k1 in mine)
+    common = {"unit": UNIT, "h2d_bytes_per_step": int(m * wa * 8 + l * wb * 8),
+              "d2h_bytes_per_step": int(m * wb * 8),
+              "h2d_bytes_per_step_rank0": int(h2d_rank),
+              "d2h_bytes_per_step_rank0": int(hcv[0].nbytes)}
+
+    def max_over_ranks(ms, ok):
+        t = torch.tensor([ms, 0.0 if ok else 1.0], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0].item()), not bool(t[1].item())
+
+    # (1) serial: upload, multiply, download, one product at a time
+    ad, bd = g.create(mr, l, dev), g.create(l, n, dev)
+
+    def e2e_step():
+        g.from_numpy(hav, l, out=ad, nonblocking=True)
+        for k0, k1 in mine:
+            g.from_numpy(hbv[k0:k1], n, out=g.window(bd, k0, 0, k1 - k0, n),
+                         nonblocking=True)
+        cc = mul_sharded(ad, bd, params, src=None, npanels=args.npanels)
+        g.core._download(cc, hcv[0], nonblocking=True)
+        return cc
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ee = []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        e2e_step()
+        e1.record(stream)
+        ee.append((e0, e1))
+    torch.cuda.synchronize()
+    ser_ms, ser_ok = max_over_ranks(
+        sum(x.elapsed_time(y) for x, y in ee) / args.steps,
+        bool(np.array_equal(hcv[0], want)))
+    serial = dict(common, value=bitops / (ser_ms * 1e-3), ms_per_step=ser_ms,
+                  verified_vs_device_result=ser_ok)
+    del ad, bd
+
+    # (2) pipelined
+    pipe = ShardedHostPipeline(mr, l, n, params, dev, npanels=args.npanels)
+    for i in range(max(2, args.warmup)):
+        pipe.submit(hav, hbv, hcv[i % 2])
+    pipe.sync()
+    torch.cuda.synchronize()
+    dist.barrier()
+    h2d, _, d2h = pipe.streams
+    steps = max(args.steps, 30)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(h2d)
+    for i in range(steps):
+        pipe.submit(hav, hbv, hcv[i % 2])
+    e1.record(d2h)
+    pipe.sync()
+    torch.cuda.synchronize()
+    pip_ms, pip_ok = max_over_ranks(
+        e0.elapsed_time(e1) / steps,
+        all(np.array_equal(x, want) for x in hcv))
+    piped = dict(common, value=bitops / (pip_ms * 1e-3), ms_per_step=pip_ms,
+                 verified_vs_device_result=pip_ok, steps=steps,
+                 mode="ShardedHostPipeline: per product each rank uploads its "
+                      "A rows and its block of B's rows from pinned host "
+                      "memory (its own PCIe link), mul_sharded(src=None) "
+                      "broadcasts the blocks over NCCL while panels multiply, "
+                      "each rank downloads its C rows; copies of neighbouring "
+                      "products overlap compute; first upload to last "
+                      "download, max over ranks")
+    return piped, serial
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -267,7 +388,13 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    dist_on = world > 1 or args.sharded
+    if dist_on:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(_free_port()))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
@@ -278,14 +405,14 @@ def main():
     m, l, n = w["m"], w["l"], w["n"]
     params = g.default_params() if not args.cutoff else \
         g.MulParams(cutoff=args.cutoff, k=8)
-    r0, r1 = shard_rows(m, world, rank) if world > 1 else (0, m)
+    r0, r1 = shard_rows(m, world, rank) if dist_on else (0, m)
     a = g.random(r1 - r0, l, w["seed_a"], device=dev, row_base=r0)
     b = g.random(l, n, w["seed_b"], device=dev) if (world == 1 or rank == 0) \
         else g.create(l, n, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 
     def step():
-        if world == 1:
+        if not dist_on:
             return g.mul_strassen(a, b, params)
         return mul_sharded(a, b, params, src=0, npanels=args.npanels)
 
@@ -295,7 +422,7 @@ def main():
         c = None                           # let the caching allocator reuse C
         c = step()
     torch.cuda.synchronize()
-    if world > 1:
+    if dist_on:
         dist.barrier()
     torch.cuda.synchronize()
 
@@ -319,12 +446,12 @@ def main():
     n_launch = g.launch_count() - n_launch0
     kern_ms, kern_ops, kern_n = _lib.timer_read()
     _lib.timer_enable(False)
-    if world > 1:
+    if dist_on:
         dist.barrier()
     torch.cuda.synchronize()
     clk = clocks.stop()
     total_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
-    if world > 1:
+    if dist_on:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
@@ -336,7 +463,7 @@ def main():
     verified = None
     if not args.no_verify and not args.size:
         words = c.to_numpy()
-        if world > 1:
+        if dist_on:
             parts = [None] * world
             dist.all_gather_object(parts, words)
             words = None
@@ -350,7 +477,10 @@ def main():
 
     # ---- end to end through the public API with pinned host buffers
     e2e = e2e_serial = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and dist_on:
+        e2e, e2e_serial = e2e_sharded(args, g, dev, stream, flush, a, r0, r1,
+                                      w, params, world, rank, c)
+    if not args.no_e2e and not dist_on:
         import numpy as np
         from paper_0811_1714_b200.pipeline import HostPipeline
         wa, wb = g.words_per_row(l), g.words_per_row(n)
@@ -431,7 +561,7 @@ def main():
                 bool(e2e_serial["verified_sha256"])
 
     if rank != 0:
-        if world > 1:
+        if dist_on:
             dist.destroy_process_group()
         return
 
@@ -508,7 +638,7 @@ def main():
                                f"Strassen-Winograd (cutoff {params.cutoff}) "
                                f"over the {args.engine} base case",
                    "m": m, "l": l, "n": n, "cutoff": params.cutoff,
-                   "parallelism": "single" if world == 1 else
+                   "parallelism": "single" if not dist_on else
                    f"rows{world} + NCCL broadcast of B ({args.npanels} panels)",
                    "l2": "flushed between timed steps (512 MiB write)"},
         "verified_sha256": verified,
@@ -525,7 +655,7 @@ def main():
         "vs_paper_2008_cpu": value / PAPER_2008_CPU,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
 
 

@@ -48,7 +48,8 @@ int main(void) {
         fprintf(stderr, "sharded product differs from gf2_strassen\n");
         return 1;
     }
-    CHECK(gf2_mul_sharded(&c, &a, &b, comm, 0, 2, 2048, 1, NULL)); /* C += A.B -> 0 */
+    /* src = -1: rank r supplies block r of B's rows (all of B on rank 0 here) */
+    CHECK(gf2_mul_sharded(&c, &a, &b, comm, -1, 2, 2048, 1, NULL)); /* C += A.B -> 0 */
     CHECK(gf2_download(&c, h1, wn, NULL));
     CHECK(gf2_stream_sync(NULL));
     for (int64_t i = 0; i < m * wn; ++i)

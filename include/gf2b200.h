@@ -56,13 +56,15 @@ const char *gf2_last_error(void);
 /* row-sharded multi-GPU C_p (+)= A_p . B for hosts that
  * run NCCL themselves (one process or thread per GPU). This rank passes its
  * row shard of C and A and a device buffer `b` for all of B (its contents
- * matter only on rank `src`); B is broadcast with ncclBroadcast in `npanels`
- * word-aligned K-panels on an internal communication stream, and each panel
- * is multiplied (Strassen-Winograd with `cutoff`) as soon as it has landed.
+ * matter only on rank `src`; with src < 0, B's rows are split into nranks
+ * word-aligned blocks and rank r supplies block r, sharded.py owned_rows);
+ * B is broadcast with ncclBroadcast on an internal communication stream and
+ * multiplied in `npanels` word-aligned K-panels (sharded.py k_panels), each
+ * (Strassen-Winograd with `cutoff`) as soon as its rows have landed.
  * `nccl_comm` is an ncclComm_t; NCCL is loaded at run time (libnccl.so.2).
- * Call it outside ncclGroupStart/End: the per-panel "landed" events are
- * recorded right after each ncclBroadcast is issued, which a group would
- * defer (a host thread driving several GPUs calls it once per device).
+ * Call it outside ncclGroupStart/End, from one host thread or process per
+ * GPU: the per-panel "landed" events are recorded right after each
+ * ncclBroadcast is issued, which a group would defer.
  * The Python package offers the same over torch.distributed
  * (paper_0811_1714_b200.sharded.mul_sharded). */
 int gf2_mul_sharded(const gf2_view *c_shard, const gf2_view *a_shard, const gf2_view *b, void *nccl_comm,

@@ -1,9 +1,10 @@
 // Row-sharded multi-GPU multiply for hosts that drive NCCL themselves
 // (the Python layer does the same over torch.distributed,
 // paper_0811_1714_b200/sharded.py). Each rank holds its row shard of A and C
-// and a device buffer for all of B; B's contents matter on the root, which
-// broadcasts it in K-panels on a communication stream while this rank
-// multiplies the panels that have landed: C_p (^)= A_p[:, panel] . B[panel, :].
+// and a device buffer for all of B; B's contents matter on the root (or, with
+// src < 0, rank r's block of rows on rank r), which broadcasts it on a
+// communication stream while this rank multiplies the K-panels that have
+// landed: C_p (^)= A_p[:, panel] . B[panel, :].
 // XOR accumulation is shard-local, so the broadcast is the only collective.
 //
 // NCCL is resolved at run time (dlopen of libnccl.so.2 -- the copy already
@@ -26,8 +27,10 @@ namespace {
 
 typedef ncclResult_t (*BroadcastFn)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
 typedef const char *(*ErrStrFn)(ncclResult_t);
+typedef ncclResult_t (*CountFn)(const ncclComm_t, int *);
 BroadcastFn g_bcast = nullptr;
 ErrStrFn g_errstr = nullptr;
+CountFn g_count = nullptr;
 
 int load_nccl() {
     if (g_bcast) return GF2_OK;
@@ -35,7 +38,9 @@ int load_nccl() {
     if (!h) return set_error(GF2_ERR_NCCL, std::string("libnccl.so.2 not loadable: ") + dlerror());
     g_bcast = (BroadcastFn)dlsym(h, "ncclBroadcast");
     g_errstr = (ErrStrFn)dlsym(h, "ncclGetErrorString");
-    if (!g_bcast) return set_error(GF2_ERR_NCCL, "ncclBroadcast not found in libnccl.so.2");
+    g_count = (CountFn)dlsym(h, "ncclCommCount");
+    if (!g_bcast || !g_count)
+        return set_error(GF2_ERR_NCCL, "ncclBroadcast / ncclCommCount not found in libnccl.so.2");
     return GF2_OK;
 }
 
@@ -87,23 +92,34 @@ int mul_sharded(const gf2_view &c, const gf2_view &a, const gf2_view &b, ncclCom
     const auto panels = k_panels(a.ncols, npanels);
     if (!accumulate) GF2_TRY(launch_zero(c, s));
     if (panels.empty()) return GF2_OK;
+    // src >= 0: one broadcast per compute panel, from rank src. src < 0: B's
+    // rows split into nranks word-aligned blocks, block r broadcast from rank
+    // r (sharded.py owned_rows); a panel waits for every block it overlaps.
+    std::vector<std::pair<int64_t, int64_t>> pieces = panels;
+    if (src < 0) {
+        int nranks = 1;
+        GF2_TRY(check_nccl(g_count(comm, &nranks), "ncclCommCount"));
+        pieces = k_panels(a.ncols, nranks);
+    }
     CommStream *cs = nullptr;
-    GF2_TRY(comm_stream(&cs, panels.size()));
+    GF2_TRY(comm_stream(&cs, pieces.size()));
     // the broadcast may overwrite B only after earlier work on `s` is done
     cudaEvent_t ready = cs->landed[0];
     GF2_TRY(check_cuda(cudaEventRecord(ready, s), "ready"));
     GF2_TRY(check_cuda(cudaStreamWaitEvent(cs->s, ready, 0), "ready wait"));
-    for (size_t i = 0; i < panels.size(); ++i) {
-        const int64_t k0 = panels[i].first, k1 = panels[i].second;
+    for (size_t i = 0; i < pieces.size(); ++i) {
+        const int64_t k0 = pieces[i].first, k1 = pieces[i].second;
         // rows k0..k1 of B, whole pitched rows: one contiguous byte range
         GF2_TRY(check_nccl(g_bcast(b.data + k0 * b.pitch, b.data + k0 * b.pitch, (size_t)((k1 - k0) * b.pitch) * 8,
-                                   ncclUint8, src, comm, cs->s),
+                                   ncclUint8, src >= 0 ? src : (int)i, comm, cs->s),
                            "ncclBroadcast"));
         GF2_TRY(check_cuda(cudaEventRecord(cs->landed[i], cs->s), "panel landed"));
     }
+    size_t next = 0;
     for (size_t i = 0; i < panels.size(); ++i) {
         const int64_t k0 = panels[i].first, k1 = panels[i].second;
-        GF2_TRY(check_cuda(cudaStreamWaitEvent(s, cs->landed[i], 0), "panel wait"));
+        for (; next < pieces.size() && pieces[next].first < k1; ++next)
+            GF2_TRY(check_cuda(cudaStreamWaitEvent(s, cs->landed[next], 0), "panel wait"));
         GF2_TRY(strassen_mul(c, sub_view(a, 0, k0, a.nrows, k1 - k0), sub_view(b, k0, 0, k1 - k0, b.ncols), cutoff,
                              1, s));
     }

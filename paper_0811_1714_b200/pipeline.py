@@ -98,3 +98,86 @@ class HostPipeline:
     @property
     def streams(self):
         return self.h2d, self.comp, self.d2h
+
+
+class ShardedHostPipeline:
+    """HostPipeline for one rank of a row-sharded multi-GPU multiply
+    (sharded.py): per product this rank uploads its rows of A and its block
+    of B's rows (`owned_rows(l, world, rank, None)`) over its own PCIe link,
+    `mul_sharded(src=None)` broadcasts every rank's block over NCCL while the
+    K-panels multiply, and the rank downloads its rows of C. Same three
+    streams, two buffer sets and event ordering as HostPipeline; every rank
+    of the group calls `submit` for every product, in the same order."""
+
+    def __init__(self, m_shard: int, l: int, n: int,
+                 params: MulParams | None = None, device=None, group=None,
+                 npanels: int = 2):
+        import torch
+        import torch.distributed as dist
+        from .sharded import owned_rows
+        self.m, self.l, self.n = m_shard, l, n
+        self.params = params or default_params()
+        self.group, self.npanels = group, npanels
+        self.device = device if device is not None else \
+            torch.device("cuda", torch.cuda.current_device())
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        self.owned = owned_rows(l, world, rank, None)
+        self.h2d = torch.cuda.Stream(self.device)
+        self.comp = torch.cuda.Stream(self.device)
+        self.d2h = torch.cuda.Stream(self.device)
+        self.sets = [(BitMatrix(m_shard, l, self.device), BitMatrix(l, n, self.device),
+                      BitMatrix(m_shard, n, self.device)) for _ in range(2)]
+        ev = lambda: torch.cuda.Event()  # noqa: E731
+        self.uploaded = [ev(), ev()]
+        self.computed = [ev(), ev()]
+        self.downloaded = [ev(), ev()]
+        self.used = [False, False]
+        self.i = 0
+
+    def submit(self, a_words: np.ndarray, b_words: np.ndarray,
+               c_out: np.ndarray) -> None:
+        """Queue C_p = A_p . B. `a_words`: this rank's rows of A; `b_words`:
+        (l, width) with at least this rank's block of rows filled (the rest
+        is not read); `c_out` receives this rank's rows of C."""
+        import torch
+        from .core import window
+        from .sharded import mul_sharded
+        HostPipeline._check(self, a_words, self.m, self.l, "A")
+        HostPipeline._check(self, b_words, self.l, self.n, "B")
+        HostPipeline._check(self, c_out, self.m, self.n, "C")
+        k = self.i % 2
+        a, b, c = self.sets[k]
+        lib = _lib.lib_cuda()
+        with torch.cuda.stream(self.h2d):
+            if self.used[k]:
+                self.h2d.wait_event(self.computed[k])      # set k consumed
+            s = self.h2d.cuda_stream
+            _lib.check(lib.gf2_upload(a._view(), a_words.ctypes.data,
+                                      a_words.strides[0] // 8, s))
+            for k0, k1 in self.owned:
+                _lib.check(lib.gf2_upload(
+                    window(b, k0, 0, k1 - k0, self.n)._view(),
+                    b_words[k0:k1].ctypes.data, b_words.strides[0] // 8, s))
+            self.uploaded[k].record(self.h2d)
+        with torch.cuda.stream(self.comp):
+            self.comp.wait_event(self.uploaded[k])
+            if self.used[k]:
+                self.comp.wait_event(self.downloaded[k])   # set k's C read out
+            mul_sharded(a, b, self.params, src=None, group=self.group,
+                        npanels=self.npanels, c=c, accumulate=False)
+            self.computed[k].record(self.comp)
+        with torch.cuda.stream(self.d2h):
+            self.d2h.wait_event(self.computed[k])
+            _lib.check(lib.gf2_download(c._view(), c_out.ctypes.data,
+                                        c_out.strides[0] // 8,
+                                        self.d2h.cuda_stream))
+            self.downloaded[k].record(self.d2h)
+        self.used[k] = True
+        self.i += 1
+
+    def sync(self) -> None:
+        self.d2h.synchronize()
+
+    @property
+    def streams(self):
+        return self.h2d, self.comp, self.d2h

@@ -53,31 +53,62 @@ def k_panels(l: int, npanels: int) -> list[tuple[int, int]]:
     return out
 
 
+def owned_rows(l: int, world: int, rank: int,
+               src: int | None) -> list[tuple[int, int]]:
+    """The rows [k0, k1) of B whose contents `rank` must supply: all of B on
+    `src`, or with src=None the word-aligned block k_panels(l, world)[rank]
+    (B's rows distributed over the ranks, e.g. each rank uploading its block
+    from host memory over its own PCIe link)."""
+    if src is not None:
+        return [(0, l)] if rank == src and l > 0 else []
+    blocks = k_panels(l, world)
+    return [blocks[rank]] if rank < len(blocks) else []
+
+
 def pipelined_broadcast(b_rows, panels: Sequence[tuple[int, int]],
                         local_addmul: Callable[[int, int], None],
-                        src: int = 0, group=None) -> None:
-    """Broadcast row panels of `b_rows` (a [l, pitch] tensor; rows = B's
-    rows) from `src` asynchronously, and run local_addmul(k0, k1) for each
-    panel as soon as it has landed."""
+                        src: int | None = 0, group=None) -> None:
+    """Broadcast the rows of `b_rows` (a [l, pitch] tensor; rows = B's rows)
+    asynchronously and run local_addmul(k0, k1) for each compute panel as
+    soon as its rows have landed. src = a rank: one broadcast per panel from
+    it. src = None: one broadcast per rank's block (owned_rows) from that
+    rank; a panel waits for every block it overlaps."""
     import torch.distributed as dist
-    works = [dist.broadcast(b_rows[k0:k1], src=src, group=group,
-                            async_op=True) for k0, k1 in panels]
-    for (k0, k1), w in zip(panels, works):
-        w.wait()
+    if not panels:
+        return
+    if src is None:
+        world = dist.get_world_size(group)
+        pieces = k_panels(panels[-1][1], world)
+        roots = list(range(len(pieces)))
+        if group is not None:  # group ranks -> global ranks
+            roots = [dist.get_global_rank(group, r) for r in roots]
+    else:
+        pieces, roots = list(panels), [src] * len(panels)
+    works = [dist.broadcast(b_rows[k0:k1], src=r, group=group, async_op=True)
+             for (k0, k1), r in zip(pieces, roots)]
+    nxt = 0
+    for k0, k1 in panels:
+        while nxt < len(pieces) and pieces[nxt][0] < k1:
+            works[nxt].wait()
+            nxt += 1
         local_addmul(k0, k1)
 
 
-def mul_sharded(a_shard, b, params=None, src: int = 0, group=None,
-                npanels: int = 2, c=None):
+def mul_sharded(a_shard, b, params=None, src: int | None = 0, group=None,
+                npanels: int = 2, c=None, accumulate: bool = True):
     """C_p (+)= A_p . B on this rank. `b` is a BitMatrix of B's full shape
-    on every rank; its contents matter only on `src`. If `c` is given the
-    product is accumulated into it (addmul), else a fresh C_p is returned."""
-    from .core import create, window
+    on every rank; its contents matter only on `src` -- or, with src=None,
+    only this rank's block of rows (`owned_rows`). If `c` is given the
+    product is accumulated into it (addmul) -- or overwrites it with
+    accumulate=False -- else a fresh C_p is returned."""
+    from .core import create, window, zero_into
     from .strassen import addmul
 
     m, l, n = a_shard.nrows, a_shard.ncols, b.ncols
     if c is None:
         c = create(m, n, a_shard.device)
+    elif not accumulate:
+        zero_into(c)
     panels = k_panels(l, npanels)
 
     def local(k0: int, k1: int) -> None:
@@ -90,4 +121,5 @@ def mul_sharded(a_shard, b, params=None, src: int = 0, group=None,
     return c
 
 
-__all__ = ["shard_rows", "k_panels", "pipelined_broadcast", "mul_sharded"]
+__all__ = ["shard_rows", "k_panels", "owned_rows", "pipelined_broadcast",
+           "mul_sharded"]

@@ -64,6 +64,19 @@ def test_sharded_cfg3_digest(nccl_group, digests):
     assert O.digest(c.to_numpy()) == digests["cfg3"]
 
 
+def test_sharded_rotating_roots_accumulate(nccl_group):
+    # src=None: panel i rooted at rank i % world (world 1 here: the same
+    # broadcasts, the rotating-root code path); C0 + A.B into a given c
+    from paper_0811_1714_b200.sharded import mul_sharded
+    m, l, n = 1100, 3000, 900
+    a, b = g.random(m, l, 3), g.random(l, n, 4)
+    c = g.random(m, n, 5)
+    mul_sharded(a, b, g.MulParams(cutoff=512), src=None, npanels=5, c=c)
+    want = O.naive_product(O.random(m, l, 3), O.random(l, n, 4)).words ^ \
+        O.random(m, n, 5).words
+    assert np.array_equal(c.to_numpy(), want)
+
+
 def test_host_pipeline_products():
     import torch
     from paper_0811_1714_b200.pipeline import HostPipeline
@@ -83,4 +96,28 @@ def test_host_pipeline_products():
     pipe.sync()
     for i, c in enumerate(outs):
         want = O.naive_product(O.random(m, l, 100 + i), O.random(l, n, 200 + i))
+        assert np.array_equal(c, want.words), i
+
+
+def test_sharded_host_pipeline_products(nccl_group):
+    # world 1: this rank owns all of B; the pipeline's stream/event ordering
+    # and the per-product broadcast + overwrite of C are what is exercised
+    import torch
+    from paper_0811_1714_b200.pipeline import ShardedHostPipeline
+    m, l, n = 1300, 2200, 1100
+    pipe = ShardedHostPipeline(m, l, n, g.MulParams(cutoff=256), npanels=3)
+    ins, outs = [], []
+    for i in range(5):
+        a = torch.empty((m, g.words_per_row(l)), dtype=torch.int64, pin_memory=True)
+        b = torch.empty((l, g.words_per_row(n)), dtype=torch.int64, pin_memory=True)
+        av, bv = a.numpy().view(np.uint64), b.numpy().view(np.uint64)
+        av[:] = O.random(m, l, 300 + i).words
+        bv[:] = O.random(l, n, 400 + i).words
+        c = np.full((m, g.words_per_row(n)), 7, dtype=np.uint64)
+        ins.append((a, b))
+        outs.append(c)
+        pipe.submit(av, bv, c)
+    pipe.sync()
+    for i, c in enumerate(outs):
+        want = O.naive_product(O.random(m, l, 300 + i), O.random(l, n, 400 + i))
         assert np.array_equal(c, want.words), i

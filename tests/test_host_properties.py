@@ -9,7 +9,7 @@ from hypothesis import strategies as st
 
 from oracle import gf2_oracle as O
 from paper_0811_1714_b200 import peel_split
-from paper_0811_1714_b200.sharded import k_panels, shard_rows
+from paper_0811_1714_b200.sharded import k_panels, owned_rows, shard_rows
 
 dims = st.one_of(st.integers(1, 300), st.integers(1, 70000),
                  st.integers(1, 1100).map(lambda k: 64 * k),
@@ -45,6 +45,19 @@ def test_k_panels_tile_k_on_word_boundaries(l, npanels):
     for (a0, a1), (b0, b1) in zip(ps, ps[1:]):
         assert a1 == b0 and a0 < a1
     assert all(k0 % 64 == 0 for k0, _ in ps)
+
+
+@settings(max_examples=300, deadline=None)
+@given(l=st.integers(0, 70000), world=st.integers(1, 8),
+       src=st.one_of(st.none(), st.integers(0, 7)))
+def test_owned_rows_partition_b(l, world, src):
+    if src is not None and src >= world:
+        src = world - 1
+    owned = [owned_rows(l, world, r, src) for r in range(world)]
+    spans = sorted(p for o in owned for p in o)
+    assert spans == (k_panels(l, world) if src is None else ([(0, l)] if l else []))
+    if src is not None:
+        assert all(not o for r, o in enumerate(owned) if r != src)
 
 
 def test_shard_rows_rejects_bad_rank():
