@@ -199,12 +199,28 @@ __global__ void __launch_bounds__(256) k_combine_t(CombineArgs p) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t w0 = (int64_t)blockIdx.x * CT_WORDS, r0 = (int64_t)blockIdx.y * CT_ROWS;
     const u64 *sb = p.src + (int64_t)blockIdx.z * p.src_stride;
-    for (int i = 0; i < 4 * CT_ROWS * CT_WORDS / 256; ++i) {
-        const int idx = threadIdx.x + 256 * i;
-        const int qd = idx / (CT_ROWS * CT_WORDS), rem = idx % (CT_ROWS * CT_WORDS);
-        const int rr = rem / CT_WORDS, ww = rem % CT_WORDS;
-        const int64_t r = r0 + rr, w = w0 + ww;
-        tile[qd][rr][ww] = (r < p.R && w < p.W) ? __ldg(sb + p.src_off[qd] + r * p.src_pitch + w) : 0;
+    // 16 loads in flight per thread before they are staged (the loop
+    // unrolled by 4 kept 4): 652 -> 627 us at cfg5. The kernel is bound by
+    // the shuffle transposes' integer work more than by its loads (a version
+    // without shared memory, 32 loads in flight per lane, ran 690 us).
+    constexpr int PER = 4 * CT_ROWS * CT_WORDS / 256, BATCH = 16;
+#pragma unroll 1
+    for (int b0 = 0; b0 < PER; b0 += BATCH) {
+        u64 v[BATCH];
+#pragma unroll
+        for (int i = 0; i < BATCH; ++i) {
+            const int idx = threadIdx.x + 256 * (b0 + i);
+            const int qd = idx / (CT_ROWS * CT_WORDS), rem = idx % (CT_ROWS * CT_WORDS);
+            const int rr = rem / CT_WORDS, ww = rem % CT_WORDS;
+            const int64_t r = r0 + rr, w = w0 + ww;
+            v[i] = (r < p.R && w < p.W) ? __ldg(sb + p.src_off[qd] + r * p.src_pitch + w) : 0;
+        }
+#pragma unroll
+        for (int i = 0; i < BATCH; ++i) {
+            const int idx = threadIdx.x + 256 * (b0 + i);
+            const int qd = idx / (CT_ROWS * CT_WORDS), rem = idx % (CT_ROWS * CT_WORDS);
+            tile[qd][rem / CT_WORDS][rem % CT_WORDS] = v[i];
+        }
     }
     __syncthreads();
     const int64_t w = w0 + warp;

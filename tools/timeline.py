@@ -4,6 +4,7 @@ then the device time per kernel name.
 
   python tools/timeline.py                 # cfg3 16384^3 mul_strassen
   python tools/timeline.py --size 65536 --addmul --summary   # cfg5
+  python tools/timeline.py --size 4096 --cutoff 1024          # cfg2
 """
 import argparse
 import collections
@@ -20,6 +21,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--size", type=int, default=16384)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--addmul", action="store_true")
+ap.add_argument("--cutoff", type=int, default=0, help="0 = device default")
 ap.add_argument("--summary", action="store_true",
                 help="only the per-kernel totals, not every launch")
 args = ap.parse_args()
@@ -29,11 +31,14 @@ a, b = g.random(n, n, 51 if n > 16384 else 31), g.random(n, n, 52 if n > 16384 e
 c = g.random(n, n, 53) if args.addmul else None
 
 
+params = g.MulParams(cutoff=args.cutoff, k=8) if args.cutoff else None
+
+
 def step():
     if args.addmul:
-        g.addmul(c, a, b)
+        g.addmul(c, a, b, params)
     else:
-        g.mul_strassen(a, b)
+        g.mul_strassen(a, b, params)
 
 
 for _ in range(2):
