@@ -136,8 +136,12 @@ def check(rc: int) -> None:
 
 
 def current_stream() -> int:
+    """Raw cudaStream_t of torch's current stream on the current device
+    (the same value as torch.cuda.current_stream().cuda_stream, without
+    building a Stream object: ~0.3 us instead of ~3.5 us per call)."""
     import torch
-    return torch.cuda.current_stream().cuda_stream
+    c = torch._C
+    return c._cuda_getCurrentRawStream(c._cuda_getDevice())
 
 
 def launch_count() -> int:

@@ -64,7 +64,7 @@ class BitMatrix:
         self.width = words_per_row(ncols)
         self.pitch = int(lib.gf2_pitch_words(ncols))
         if device is None:
-            device = torch.device("cuda", torch.cuda.current_device())
+            device = torch._C._cuda_getDevice()  # index on the current device
         if _overwritten and self.pitch == self.width and ncols % 64 == 0:
             # a product target whose every word the kernels overwrite whole
             # (no padding words, no partial last word to merge into): no fill
@@ -230,9 +230,16 @@ def _stream():
 
 
 def _check_cuda_dev(*mats):
-    devs = {m.device for m in mats}
-    if len(devs) > 1:
-        raise DimensionError(f"operands live on different devices: {devs}")
+    # device indices, compared without building torch.device objects
+    d0 = _storage(mats[0]).get_device()
+    for m in mats[1:]:
+        if _storage(m).get_device() != d0:
+            devs = {str(x.device) for x in mats}
+            raise DimensionError(f"operands live on different devices: {devs}")
+
+
+def _storage(m):
+    return m.storage if isinstance(m, BitMatrix) else m.parent.storage
 
 
 # ------------------------------------------------------------ constructors

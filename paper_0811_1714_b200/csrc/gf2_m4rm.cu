@@ -3,14 +3,15 @@
 // Restates m4rm.py:77-121 (`_mul_into`) + graycode.py:108-156
 // (`make_table`) for the B200 memory hierarchy:
 //
-//   * A CTA owns a C tile of BM = 32*RPT rows x 1024 columns (16 words) and
+//   * A CTA owns a C tile of BM = 64*RPT rows x 1024 columns (16 words) and
 //     keeps it in registers for the whole K loop: each thread holds a
 //     128-bit column slice of RPT rows (8 lanes = one 128-byte row, so the
 //     4 quarter-warps of a warp cover 4 rows per instruction).
-//   * K advances one 64-bit word of A (64 rows of B) per stage. The B panel
-//     (64 rows x 1024 columns, 8 KiB) and the A column words (BM x 8 B) of
-//     the NEXT stage are prefetched with cp.async while the current stage is
-//     consumed (double-buffered).
+//   * K advances two 64-bit words of A (128 rows of B) per stage. The B
+//     panel (128 rows x 1024 columns, 16 KiB) and the A column words
+//     (BM x 16 B) of the NEXT stage are prefetched (TMA, or cp.async for
+//     8-byte-aligned windows) while the current stage is consumed
+//     (double-buffered).
 //   * Each half stage (32 rows of B) builds 4 Gray-code tables of 2^8 rows
 //     x 1024 bits (4 x 32 KiB) in shared memory. Table j, slot x holds the
 //     XOR of rows i of the 8-row group with bit (7-i) of x set -- exactly
@@ -31,6 +32,8 @@
 // table builds add 2^8/BM of that traffic. The kernel is bound by the
 // 128 B/clk/SM shared-memory crossbar.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "gf2_internal.cuh"
@@ -53,6 +56,12 @@ constexpr int kBStageBytes = kStageRows * kRowBytes;  // 16 KiB
 template <int RPT>
 constexpr int smem_bytes() {
     return kTables * kTableBytes + 2 * kBStageBytes + 2 * (kRowGroups * RPT) * 8 * kStageWords + 16;
+}
+
+// rows per TMA box of A words (the host encodes the map with the same box)
+template <int RPT>
+constexpr int a_box_rows() {
+    return kRowGroups * RPT < 256 ? kRowGroups * RPT : 256;
 }
 
 struct KArgs {
@@ -118,13 +127,15 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
 
 // C tile: BM = 64*RPT rows x 1024 columns, in registers. TMA: operands are
 // 16-byte aligned with 16-byte pitches, so thread 0 stages each B panel
-// (128 rows x 16 words) and the A words (BM rows x 2 words, 256-row boxes)
+// (128 rows x 16 words) and the A words (BM rows x 2 words, boxes of
+// min(BM, 256) rows)
 // with cp.async.bulk.tensor onto one mbarrier per buffer (zero fill past the
 // matrix edges); otherwise every thread issues 8-byte cp.async.
 template <int RPT, bool TMA>
 __global__ void __launch_bounds__(kThreads, 1)
     k_m4rm(KArgs p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
     constexpr int BM = kRowGroups * RPT;
+    constexpr int kABox = a_box_rows<RPT>();
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t s_tab = (uint32_t)__cvta_generic_to_shared(smem);
     const uint32_t s_bst = s_tab + kTables * kTableBytes;
@@ -162,8 +173,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_expect(bar, kBStageBytes + BM * 16);
                 tma_3d(bdst, &tmB, (int)col_w0, (int)(kw * 64), (int)prob, bar);
 #pragma unroll
-                for (int i = 0; i < BM / 256; ++i)
-                    tma_3d(s_ast + (buf * BM + 256 * i) * 16, &tmA, (int)kw, (int)(row0 + 256 * i), (int)prob, bar);
+                for (int i = 0; i < BM / kABox; ++i)
+                    tma_3d(s_ast + (buf * BM + kABox * i) * 16, &tmA, (int)kw, (int)(row0 + kABox * i), (int)prob,
+                           bar);
             }
         } else {
 #pragma unroll
@@ -368,9 +380,9 @@ void timer_end(int idx, cudaStream_t s) {
 
 int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     if (!b.m || !b.n || !b.nprob) return GF2_OK;
-    // gridDim.z = K splits (<= 8) x problems must stay <= 65535: deep
+    // gridDim.z = K splits (<= 16) x problems must stay <= 65535: deep
     // recursions (7^6 leaves at cutoff 64) run their leaves in chunks
-    constexpr int64_t kMaxBatch = 65535 / 8;
+    constexpr int64_t kMaxBatch = 65535 / 16;
     if (b.nprob > kMaxBatch) {
         for (int64_t q0 = 0; q0 < b.nprob; q0 += kMaxBatch) {
             M4rmBatch c = b;
@@ -397,34 +409,59 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     if (b.l == 0) return b.accumulate ? GF2_OK : zero_c();
 
     const int64_t col_tiles = (Wn + kTileWords - 1) / kTileWords;
-    const int64_t want = num_sms();  // one CTA per SM is resident (smem-bound)
+    const int64_t sms = num_sms();  // one CTA per SM is resident (smem-bound)
+    // Geometry from a shared-memory cost model (units: KiB of shared traffic
+    // per CTA and half stage of 32 B rows): the table build moves ~192 KiB
+    // whatever the tile height (4 tables x 256 slots x 128 B of stores plus
+    // the source rows), the lookups 34 KiB per RPT (RPT rows per thread:
+    // one 4-byte A load and four 128 B table rows per row group). A CTA runs
+    // 2 half stages per A word of its K range plus a fixed cost (launch,
+    // first stage in flight, epilogue) of about one half stage; CTAs run in
+    // waves of one per SM. A K split also costs the zeroing pass and
+    // red.xor. Large products keep RPT 16 (BM 1024) and split K only to fill
+    // waves (16384^3: 256 tiles, 4 splits, 6.92 waves); small ones
+    // (cfg1 1024^3) trade taller tiles for more CTAs with shorter K ranges.
     int rpt = 16;
-    int64_t row_tiles = (b.m + kRowGroups * rpt - 1) / (kRowGroups * rpt);
-    while (rpt > 4 && row_tiles * col_tiles * b.nprob < want) {
-        rpt /= 2;
-        row_tiles = (b.m + kRowGroups * rpt - 1) / (kRowGroups * rpt);
-    }
-    const int64_t tiles = row_tiles * col_tiles * b.nprob;
-    // split K so the CTA count fills whole waves of resident CTAs (one per
-    // SM): efficiency(n) = T n / (S ceil(T n / S)). A split costs a zeroing
-    // pass and red.xor accumulation, hence the small penalty. (16384^3:
-    // 256 tiles -> 1.73 waves at n = 1, 6.92 waves / 98.8 % at n = 4.)
-    auto wave_eff = [&](int64_t n) {
-        const int64_t ctas = tiles * n;
-        return (double)ctas / (double)(want * ((ctas + want - 1) / want));
-    };
     int nsplit = 1;
-    double best = wave_eff(1);
-    for (int64_t n = 2; n <= 8 && n <= (Wl + 1) / 2; ++n) {
-        const double e = wave_eff(n) - 0.02;
-        if (e > best + 1e-9) {
-            best = e;
-            nsplit = (int)n;
+    int64_t kws = Wl;
+    {
+        double best = 0;
+        for (int r : {16, 8, 4, 2}) {
+            const int64_t rt = (b.m + kRowGroups * r - 1) / (kRowGroups * r);
+            const int64_t tiles = rt * col_tiles * b.nprob;
+            for (int64_t n = 1; n <= 16 && n <= Wl; ++n) {
+                // A words per split: even, so every split starts its TMA
+                // boxes on a 16-byte boundary (a box at an odd word faults)
+                int64_t w = (Wl + n - 1) / n;
+                if (w < Wl) w = (w + 1) & ~int64_t(1);
+                const int64_t ns = (Wl + w - 1) / w;  // splits actually used
+                if (ns != n) continue;
+                const int64_t ctas = tiles * ns;
+                const int64_t waves = (ctas + sms - 1) / sms;
+                const double per_cta = (2.0 * (double)w + 1.0) * (192.0 + 34.0 * r);
+                const double cost = (double)waves * per_cta * (ns > 1 ? 1.02 : 1.0);
+                if (best == 0 || cost < best * 0.999) {
+                    best = cost;
+                    rpt = r;
+                    nsplit = (int)ns;
+                    kws = w;
+                }
+            }
         }
     }
-    int64_t kws = (Wl + nsplit - 1) / nsplit;
-    kws = (kws + kStageWords - 1) / kStageWords * kStageWords;  // splits start on a stage
-    nsplit = (int)((Wl + kws - 1) / kws);
+    {
+        // tuning override, GF2_M4RM_GEOM="rpt,nsplit" (tools/ only)
+        static const char *geom = getenv("GF2_M4RM_GEOM");
+        int r = 0, n = 0;
+        if (geom && sscanf(geom, "%d,%d", &r, &n) == 2 && (r == 2 || r == 4 || r == 8 || r == 16) && n >= 1 &&
+            n <= 16) {
+            rpt = r;
+            kws = (Wl + n - 1) / n;
+            if (kws < Wl) kws = (kws + 1) & ~int64_t(1);
+            nsplit = (int)((Wl + kws - 1) / kws);
+        }
+    }
+    const int64_t row_tiles = (b.m + kRowGroups * rpt - 1) / (kRowGroups * rpt);
     if ((int64_t)nsplit * b.nprob > 65535 || row_tiles > 65535)
         return set_error(GF2_ERR_PARAMETER, "m4rm grid too large");
 
@@ -444,7 +481,7 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
         // words x rows x problems; the problem stride is unused when nprob == 1
         const uint64_t da[3] = {(uint64_t)Wl, (uint64_t)b.m, (uint64_t)b.nprob};
         const uint64_t sa[2] = {(uint64_t)b.pa * 8, (uint64_t)(b.nprob > 1 ? b.sa : b.m * b.pa) * 8};
-        const uint32_t ba[3] = {2, 256, 1};
+        const uint32_t ba[3] = {2, (uint32_t)std::min(kRowGroups * rpt, 256), 1};
         const uint64_t db[3] = {(uint64_t)Wn, (uint64_t)b.l, (uint64_t)b.nprob};
         const uint64_t sb[2] = {(uint64_t)b.pb * 8, (uint64_t)(b.nprob > 1 ? b.sb : b.l * b.pb) * 8};
         const uint32_t bb[3] = {(uint32_t)kTileWords, (uint32_t)kStageRows, 1};
@@ -458,9 +495,12 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     else if (rpt == 8)
         rc = tma ? launch_rpt<8, true>(ka, ta, tb, col_tiles, row_tiles, z, s)
                  : launch_rpt<8, false>(ka, ta, tb, col_tiles, row_tiles, z, s);
-    else
+    else if (rpt == 4)
         rc = tma ? launch_rpt<4, true>(ka, ta, tb, col_tiles, row_tiles, z, s)
                  : launch_rpt<4, false>(ka, ta, tb, col_tiles, row_tiles, z, s);
+    else
+        rc = tma ? launch_rpt<2, true>(ka, ta, tb, col_tiles, row_tiles, z, s)
+                 : launch_rpt<2, false>(ka, ta, tb, col_tiles, row_tiles, z, s);
     timer_end(tidx, s);
     return rc;
 }
