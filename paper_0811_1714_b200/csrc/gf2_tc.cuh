@@ -90,6 +90,19 @@ __device__ __forceinline__ bool elect_one() {
                    "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                          \
                  : "r"(taddr))
 
+// tcgen05.wait::ld that also "produces" r[0..31], so the compiler cannot
+// move reads of a TMEM_LD32 destination above the wait (the load is
+// asynchronous; its destination registers are only valid after the wait).
+#define TMEM_WAIT_LD32(r)                                                                                      \
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n"                                                           \
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),        \
+                   "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]),    \
+                   "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), \
+                   "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), \
+                   "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])                                          \
+                 :                                                                                             \
+                 : "memory")
+
 #define TMEM_LD16(taddr, r)                                                                                    \
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, " \
                  "[%16];\n"                                                                                     \
@@ -209,10 +222,16 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 }
 
 // arrive on the leader CTA's copy of a barrier (cluster scope)
+// Arrive on the leader CTA's copy of `bar` (accumulator-free barriers). The
+// epilogue threads that arrive have already completed their TMEM reads
+// (tcgen05.wait::ld) and fenced them (tcgen05.fence::before_thread_sync),
+// so the arrive needs no release semantics: a release arrive would also wait
+// for the thread's outstanding red.xor stores to C (MEMBAR), putting a
+// global-memory round trip on every tile's accumulator hand-back.
 __device__ __forceinline__ void mbar_arrive_leader(uint32_t bar) {
     uint32_t remote;
     asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(remote) : "r"(bar));
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote) : "memory");
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote) : "memory");
 }
 
 

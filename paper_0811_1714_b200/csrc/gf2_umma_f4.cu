@@ -413,19 +413,31 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
             const uint32_t acc_phase = (it >> 1) & 1;
             mbar_wait(bar_tfull + 8 * acc, acc_phase);
             tc_fence_after();
+            // 32-column groups, software-pipelined: group c+1's TMEM load is
+            // in flight while group c's parities are packed. Packing has no
+            // serial chain: each column's parity is shifted into place on its
+            // own and OR-ed into one of 4 partial words (4-deep LOP3 chains
+            // instead of a 64-deep shift-or chain per group), so small-K tiles
+            // are no longer epilogue-bound.
+            const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * F4_BN;
             uint32_t packed[F4_BN / 32];
+            uint32_t vb[2][32];
+            TMEM_LD32(trow, vb[0]);
+            TMEM_WAIT_LD32(vb[0]);
 #pragma unroll
             for (int c = 0; c < F4_BN / 32; ++c) {
                 packed[c] = 0;
                 if (c < nch) {
-                    uint32_t v[32];
-                    TMEM_LD32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * F4_BN + c * 32, v);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                    uint32_t pk = 0;
+                    if (c + 1 < nch) TMEM_LD32(trow + (c + 1) * 32, vb[(c + 1) & 1]);
+                    const uint32_t *v = vb[c & 1];
+                    uint32_t part[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        pk = (pk << 1) | (__float_as_uint(__uint_as_float(v[j]) + 8388608.0f) & 1u);
-                    packed[c] = pk;
+                    for (int j = 0; j < 32; ++j) {
+                        const uint32_t u = __float_as_uint(__uint_as_float(v[j]) + 8388608.0f);
+                        part[j & 3] |= (u << (31 - j)) & (1u << (31 - j));
+                    }
+                    packed[c] = (part[0] | part[1]) | (part[2] | part[3]);
+                    if (c + 1 < nch) TMEM_WAIT_LD32(vb[(c + 1) & 1]);
                 }
             }
             tc_fence_before();
