@@ -168,6 +168,7 @@ struct UArgs {
     int post;
     int64_t qoffC[4];
     unsigned post_mask[7];
+    int dbg;  // timing experiments only (GF2_F4_DBG): 1 no C stores, 2 no epilogue work
 };
 
 template <int CG>

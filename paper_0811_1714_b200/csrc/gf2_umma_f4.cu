@@ -26,7 +26,9 @@ constexpr int F4_BNH = F4_BN / 2;          // B rows per CTA of a pair
 constexpr int F4_STG = 7;
 constexpr int F4_A_ST = BM * BK;           // 128 rows x 128 B (256 K entries)
 constexpr int F4_B_ST = F4_BNH * BK;       // 112 rows x 128 B
-constexpr int F4_SMEM = F4_STG * (F4_A_ST + F4_B_ST) + 2048;
+constexpr int F4_EPI_OFF = 256;            // epilogue staging, after the barriers
+constexpr int F4_EPI_BYTES = 4 * 32 * 4 * 8;  // 4 warps x 32 rows x 4 words
+constexpr int F4_SMEM = F4_STG * (F4_A_ST + F4_B_ST) + 1024 + F4_EPI_OFF + F4_EPI_BYTES;
 constexpr int F4_SF_COL = 2 * F4_BN;       // TMEM columns 448..511: constant scale factors
 constexpr int64_t F4_KCHUNK = 8192;
 static_assert(F4_SMEM <= 232448, "k_umma_f4 shared memory");
@@ -266,6 +268,63 @@ __device__ __forceinline__ void store_row_f4(const UArgs &p, const uint32_t *pac
     }
 }
 
+// XOR-accumulate a warp's 32 rows of a tile (packed[c] = 32-bit group g0+c
+// of this lane's row) into C, coalesced: the row's 64-bit words ws..ws+3
+// (ws = g0/2; a group outside the tile contributes a zero half, a no-op under
+// XOR) are staged in shared memory, then each red.xor.b64 instruction covers
+// 8 rows x 4 consecutive words, so the L2 sees one or two 32-byte sectors
+// per row instead of 4 separate 8-byte requests. Products of the fused last
+// Strassen level go to every C quadrant in their post mask.
+__device__ __forceinline__ void xor_rows_f4(const UArgs &p, const uint32_t *packed, uint32_t stg, int64_t row0,
+                                            int64_t g0, int nch, int64_t gprob, int lane) {
+    uint32_t v[F4_BN / 32 + 1];
+#pragma unroll
+    for (int c = 0; c < F4_BN / 32; ++c) {
+        const int64_t rem = p.n - (g0 + c) * 32;
+        uint32_t x = (c < nch && rem > 0) ? packed[c] : 0u;
+        if (rem > 0 && rem < 32) x &= ~(~0u >> rem);  // columns >= n stay untouched
+        v[c] = x;
+    }
+    v[F4_BN / 32] = 0u;
+    u64 w[4];
+    if ((g0 & 1) == 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = ((u64)v[2 * k] << 32) | v[2 * k + 1];
+    } else {
+        w[0] = v[0];
+#pragma unroll
+        for (int k = 1; k < 4; ++k) w[k] = ((u64)v[2 * k - 1] << 32) | v[2 * k];
+    }
+    asm volatile("st.shared.v2.u64 [%0], {%1, %2};\n" ::"r"(stg + lane * 32), "l"(w[0]), "l"(w[1]) : "memory");
+    asm volatile("st.shared.v2.u64 [%0], {%1, %2};\n" ::"r"(stg + lane * 32 + 16), "l"(w[2]), "l"(w[3]) : "memory");
+    __syncwarp();
+    const int64_t ws = g0 >> 1;
+    const int64_t nw = ((g0 + nch - 1) >> 1) - ws + 1;  // words this tile touches (<= 4)
+    const int k = lane & 3;
+    u64 x[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        asm volatile("ld.shared.u64 %0, [%1];\n" : "=l"(x[i]) : "r"(stg + (8 * i + (lane >> 2)) * 32 + k * 8) : "memory");
+    __syncwarp();  // the next tile's staging overwrites this buffer
+    auto red = [&](u64 *base) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t row = row0 + 8 * i + (lane >> 2);
+            if (row < p.m && k < nw && x[i])
+                atomicXor(reinterpret_cast<unsigned long long *>(base + row * p.pc + ws + k), (unsigned long long)x[i]);
+        }
+    };
+    if (p.post) {
+        const unsigned dm = p.post_mask[gprob % 7];
+        u64 *cbase = p.C + (gprob / 7) * p.sc;
+#pragma unroll
+        for (int Q = 0; Q < 4; ++Q)
+            if (dm & (1u << Q)) red(cbase + p.qoffC[Q]);
+    } else {
+        red(p.C + gprob * p.sc);
+    }
+}
+
 // Persistent CTA-pair kernel (cluster of 2, tcgen05.mma.cta_group::2), tiles
 // 256 x (32..224), 128 B = 256 K entries per stage. TMEM: accumulators at columns 0 and 224, scale factors
 // (all 0x7F) at 448..511 in both CTAs.
@@ -279,6 +338,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
     const uint32_t bar_full = sBar, bar_empty = sBar + 8 * F4_STG, bar_tfull = sBar + 16 * F4_STG,
                    bar_tempty = bar_tfull + 16;
     const uint32_t tmem_holder = bar_tempty + 16;
+    const uint32_t sEpi = sBar + F4_EPI_OFF;
     unsigned char *gen_base = smem_raw + (base_u32 - smem_u32(smem_raw));
     volatile uint32_t *tmem_holder_ptr = reinterpret_cast<volatile uint32_t *>(gen_base + (tmem_holder - base_u32));
 
@@ -419,6 +479,11 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
             // own and OR-ed into one of 4 partial words (4-deep LOP3 chains
             // instead of a 64-deep shift-or chain per group), so small-K tiles
             // are no longer epilogue-bound.
+            if (p.dbg == 2) {
+                tc_fence_before();
+                mbar_arrive_leader(bar_tempty + 8 * acc);
+                continue;
+            }
             const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * F4_BN;
             uint32_t packed[F4_BN / 32];
             uint32_t vb[2][32];
@@ -443,6 +508,11 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
             tc_fence_before();
             mbar_arrive_leader(bar_tempty + 8 * acc);
             const int64_t row = (int64_t)mtile * 256 + (int64_t)rank * BM + q * 32 + lane;
+            if (p.dbg == 1) continue;
+            if (p.post || p.mode >= 1) {
+                xor_rows_f4(p, packed, sEpi + q * 1024, row - lane, tile_g0(ntile), nch, p.q0 + prob, lane);
+                continue;
+            }
             store_row_f4(p, packed, row, (int64_t)tile_g0(ntile), nch, p.q0 + prob);
         }
     }
@@ -551,6 +621,8 @@ int launch_umma_f4(const UmmaJob &jb, int64_t nprob, cudaStream_t s) {
     ua.kchunk_blocks = (int)(F4_KCHUNK / (2 * BK));
     ua.nchunks = (ua.kblocks + ua.kchunk_blocks - 1) / ua.kchunk_blocks;
     ua.post = jb.fuse_post;
+    static const int f4dbg = getenv("GF2_F4_DBG") ? atoi(getenv("GF2_F4_DBG")) : 0;
+    ua.dbg = f4dbg;
     int rc = GF2_OK;
     if (jb.fuse_post) {
         ua.qoffC[1] = jb.n / 64; ua.qoffC[2] = jb.m * jb.pc; ua.qoffC[3] = ua.qoffC[1] + ua.qoffC[2];
