@@ -1,5 +1,6 @@
 // Internal declarations shared by the gf2b200 translation units.
 #pragma once
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -158,7 +159,19 @@ extern int g_engine;
 // 2560^3 (1.7e10) 84 vs 53 us. The automatic dispatch (Strassen leaves,
 // small non-recursive products) routes by this total work. The 8-bit
 // engines move twice the operand bytes and cross over later (2^34).
-inline double tensor_min_work() { return g_engine == 3 ? 1.0e10 : 17179869184.0; }
+// smallest product (or batch of leaves), in bit-ops, that goes to the tensor
+// engine instead of M4RM; GF2_TC_MIN_WORK overrides it (tools/ crossover runs)
+inline double tensor_min_work() {
+    static const double env = getenv("GF2_TC_MIN_WORK") ? atof(getenv("GF2_TC_MIN_WORK")) : 0.0;
+    if (env > 0) return env;
+    return g_engine == 3 ? 1.0e10 : 17179869184.0;
+}
+// smallest leaf side for tensor-core Strassen leaves (GF2_TC_MIN_LEAF
+// overrides it; tests use 256 to drive 117649 tensor leaves through chunking)
+inline int64_t tensor_min_leaf() {
+    static const int64_t env = getenv("GF2_TC_MIN_LEAF") ? atoll(getenv("GF2_TC_MIN_LEAF")) : 0;
+    return env > 0 ? env : 1024;
+}
 inline int launch_product(const M4rmBatch &b, cudaStream_t s) {
     const double work = (double)b.m * (double)b.l * (double)b.n * (double)b.nprob;
     if (g_engine == 0 || work < tensor_min_work()) return launch_m4rm(b, s);

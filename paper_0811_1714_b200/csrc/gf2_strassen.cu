@@ -226,11 +226,14 @@ int strassen_core(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0, in
                   cudaStream_t s) {
     if (g_engine != 0) {
         // tensor-core leaves when the batch is big enough to amortize the
-        // expansion and each leaf is at least one 256-row x 256-column tile
+        // expansion and each leaf is at least 1024 on every side (smaller
+        // leaves run faster on M4RM: 3000^3 at cutoff 512, 138 vs 154 us,
+        // tools/engine_cross.py)
         const int64_t lm = A0.nrows >> depth, ll = A0.ncols >> depth, ln = B0.ncols >> depth;
         double leaf = (double)lm * (double)ll * (double)ln;
         for (int i = 0; i < depth; ++i) leaf *= 7.0;
-        if (leaf >= tensor_min_work() && lm >= 256 && ln >= 256 && ll >= 256)
+        const int64_t ml = tensor_min_leaf();
+        if (leaf >= tensor_min_work() && lm >= ml && ln >= ml && ll >= ml)
             return strassen_core_tc(C0, A0, B0, depth, accumulate, s);
     }
     int64_t M[24], L[24], N[24], Lw[24], Nw[24], P[24];

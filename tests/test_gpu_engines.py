@@ -246,11 +246,26 @@ def test_deep_recursion_many_leaves(engine):
 @pytest.mark.parametrize("engine", ["tc-f4", "tc-i8"])
 def test_cfg3_depth6_tensor_leaves_chunked(engine, digests):
     """cfg3 at cutoff 256: depth 6, 117649 tensor-core leaves of 256^3 --
-    the tensor job runs in chunks of source problems."""
-    g.set_engine(engine)
-    a, b = g.random(16384, 16384, 31), g.random(16384, 16384, 32)
-    c = g.mul_strassen(a, b, g.MulParams(cutoff=256, k=8))
-    assert O.digest(words(c)) == digests["cfg3"]
+    the tensor job runs in chunks of source problems. Leaves below 1024 go
+    to M4RM by default, so GF2_TC_MIN_LEAF=256 (read once per process,
+    hence a subprocess) forces them onto the tensor engine."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import paper_0811_1714_b200 as g\n"
+        "from oracle import gf2_oracle as O\n"
+        "g.set_engine(%r)\n"
+        "a, b = g.random(16384, 16384, 31), g.random(16384, 16384, 32)\n"
+        "print(O.digest(g.mul_strassen(a, b, g.MulParams(cutoff=256, k=8)).to_numpy()))\n"
+    ) % (root, engine)
+    env = dict(os.environ, GF2_TC_MIN_LEAF="256")
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root,
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.strip().splitlines()[-1] == digests["cfg3"]
 
 
 @pytest.mark.parametrize("engine", ["tc-f4", "m4rm"])
