@@ -596,8 +596,11 @@ def main():
             "achieved": ach, "peak": peak, "unit": "TFLOP/s",
             "frac": ach / peak, "traffic": None,
             "peak_source": ("nominal dense fp4 9 PFLOP/s" if f4 else "nominal dense fp8/int8 4.5 PFLOP/s")
-                           + " (B200_PROFILING.md); MEASURED_PEAKS bf16 x2 = "
-                           f"{2 * float(peaks.get('bf16_tflops', 0)):.0f} TFLOP/s",
+                           + " (B200_PROFILING.md table; frac is 'of nominal': MEASURED_PEAKS has no "
+                           "4/8-bit figure). For scale, MEASURED_PEAKS bf16 burst x "
+                           + ("4" if f4 else "2") + " (operand-width rate ratio) = "
+                           f"{(4 if f4 else 2) * float(peaks.get('bf16_tflops', 0)):.0f} TFLOP/s; "
+                           "the higher nominal denominator is the conservative one",
         }
     if roofline is not None:
         roofline.update({
