@@ -64,7 +64,14 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
         Nw[i] = N[i] / kWordBits;
         P[i] = i == 0 ? 1 : P[i - 1] * 7;
     }
-    const int last = depth - 1;               // deepest materialized C level
+    // Post-additions of the last level fused into the GEMM epilogue (red.xor
+    // into C_{d-1}) unless the leaves are shallow in K: below
+    // GF2_POST_FUSE_MIN_K the leaf products are stored plainly into C_d and
+    // one more combine pass folds them up (red.xor traffic, not MMA time,
+    // bounds short-K tiles).
+    static const int64_t post_min_k = getenv("GF2_POST_FUSE_MIN_K") ? atoll(getenv("GF2_POST_FUSE_MIN_K")) : 0;
+    const bool fpost = L[depth] >= post_min_k;
+    const int last = fpost ? depth - 1 : depth;  // deepest materialized C level
     // pre-addition levels fused into the expansion (GF2_FUSE_LEVELS=2 folds
     // two levels into it; one is faster on B200)
     static const int fuse_env = getenv("GF2_FUSE_LEVELS") ? atoi(getenv("GF2_FUSE_LEVELS")) : 1;
@@ -177,13 +184,14 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
             if (!accumulate) rc = launch_zero(C0, s);
         } else {
             jb.C = ws + offC[last]; jb.pc = Nw[last]; jb.sc = M[last] * Nw[last];
-            rc = check_cuda(cudaMemsetAsync(ws + offC[last], 0, (size_t)(P[last] * M[last] * Nw[last]) * 8, s),
-                            "zero C_{d-1}");
+            if (fpost)  // red.xor targets start from zero; plain stores overwrite
+                rc = check_cuda(cudaMemsetAsync(ws + offC[last], 0, (size_t)(P[last] * M[last] * Nw[last]) * 8, s),
+                                "zero C_{d-1}");
         }
         jb.m = M[depth]; jb.l = L[depth]; jb.n = N[depth];
         jb.nsrc = P[lastA];
         jb.fuse_pre = fp;
-        jb.fuse_post = 1;
+        jb.fuse_post = fpost ? 1 : 0;
         for (int i = 0; i < 7; ++i) {
             jb.maskA[i] = kSA[i];
             jb.maskB[i] = bt ? swap12(kSB[i]) : kSB[i];

@@ -707,7 +707,7 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
             UmmaJob c = jb;
             c.A += s0 * jb.sa;
             c.B += s0 * jb.sb;
-            c.C += s0 * jb.sc;
+            c.C += s0 * (jb.fuse_post ? 1 : per_src) * jb.sc;  // C per source (fused post) or per leaf
             c.nsrc = std::min<int64_t>(max_src, jb.nsrc - s0);
             GF2_TRY(launch_umma_job(c, kind, s));
         }

@@ -231,6 +231,43 @@ def test_two_fused_levels_option(engine, digests):
     assert out.stdout.strip().splitlines()[-1] == digests["cfg3"]
 
 
+@pytest.mark.parametrize("engine", ["tc-f4", "tc-i8"])
+def test_unfused_post_additions(engine, digests):
+    """GF2_POST_FUSE_MIN_K above the leaf depth (read once per process,
+    hence a subprocess): the leaf products are stored plainly into their own
+    level and one more combine pass folds them up, instead of the GEMM
+    epilogue XORing each product into its destination quadrants. cfg2 at the
+    reference's cutoff (depth 2) and an accumulate into a window."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import numpy as np\n"
+        "import paper_0811_1714_b200 as g\n"
+        "from oracle import gf2_oracle as O\n"
+        "g.set_engine(%r)\n"
+        "a, b = g.random(4096, 4096, 21), g.random(4096, 4096, 22)\n"
+        "print(O.digest(g.mul_strassen(a, b, g.MulParams(cutoff=1024, k=8)).to_numpy()))\n"
+        "big = g.random(4200, 4300, 5)\n"
+        "before = big.to_numpy().copy()\n"
+        "w = g.window(big, 7, 64, 4096, 4096)\n"
+        "g.addmul(w, a, b, g.MulParams(cutoff=1024, k=8))\n"
+        "ref = g.mul_strassen(a, b).to_numpy()\n"
+        "after = big.to_numpy()\n"
+        "exp = before.copy(); exp[7:7 + 4096, 1:1 + 64] ^= ref\n"
+        "print(bool((after == exp).all()))\n"
+    ) % (root, engine)
+    env = dict(os.environ, GF2_POST_FUSE_MIN_K="1000000")
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root,
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = out.stdout.strip().splitlines()
+    assert lines[-2] == digests["cfg2"]
+    assert lines[-1] == "True"
+
+
 @pytest.mark.parametrize("engine", ["m4rm", "tc-f4"])
 def test_deep_recursion_many_leaves(engine):
     """Fuzzer regression: cutoff 64 on 4546x12000x12000 recurses to depth 6
