@@ -348,3 +348,53 @@ def test_native_code_is_what_runs():
     before = g.launch_count()
     g.mul_m4rm(g.random(64, 64, 1), g.random(64, 64, 2), 8)
     assert g.launch_count() > before
+
+
+M4RM_GEOM_CASE = r"""
+import sys; sys.path.insert(0, %(root)r)
+import numpy as np
+import paper_0811_1714_b200 as g
+from oracle import gf2_oracle as O
+from oracle import gf2_port as P
+P.set_threads(P.max_threads())
+bad = []
+for (m, l, n, seed) in [(1000, 1100, 1300, 1), (130, 2049, 777, 2), (2100, 640, 1024, 3), (64, 70, 65, 4)]:
+    pa, pb = O.random(m, l, seed), O.random(l, n, seed + 100)
+    want = P.mul_strassen(pa, pb, cutoff=1 << 20).words
+    a, b = g.random(m, l, seed), g.random(l, n, seed + 100)
+    if not np.array_equal(g.mul_m4rm(a, b, 8).to_numpy(), want):
+        bad.append(("aligned", m, l, n))
+    # odd word offsets: 8-byte staging instead of TMA
+    big_a, big_b = g.random(m + 3, l + 64, seed + 7), g.random(l + 5, n + 128, seed + 8)
+    aw, bw = g.window(big_a, 3, 64, m, l), g.window(big_b, 5, 64, l, n)
+    ha, hb = big_a.to_numpy(), big_b.to_numpy()
+    wa = O.HostMat(m, l, np.ascontiguousarray(ha[3:3 + m, 1:1 + O.words_per_row(l)]))
+    wb = O.HostMat(l, n, np.ascontiguousarray(hb[5:5 + l, 1:1 + O.words_per_row(n)]))
+    wa.words[:, -1] &= np.uint64(O.tail_mask(l))
+    wb.words[:, -1] &= np.uint64(O.tail_mask(n))
+    want_w = P.mul_strassen(wa, wb, cutoff=1 << 20).words
+    c = g.random(m, n, seed + 9)
+    c0 = c.to_numpy().copy()
+    g.mul_m4rm_into(c, aw, bw, 8)
+    if not np.array_equal(c.to_numpy(), c0 ^ want_w):
+        bad.append(("window-accumulate", m, l, n))
+print("BAD", bad)
+"""
+
+
+@pytest.mark.parametrize("geom", ["16,1", "16,3", "8,5", "4,16", "2,8", "2,16"])
+def test_m4rm_every_geometry(geom):
+    """Every k_m4rm tile height (RPT 16/8/4/2 -> 1024/512/256/128 rows) and
+    K-split count, forced through GF2_M4RM_GEOM (read once per process,
+    hence a subprocess), on ragged shapes with the TMA path (aligned
+    operands) and the 8-byte cp.async path (odd word offsets), plain and
+    accumulating, against the C port."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GF2_M4RM_GEOM=geom)
+    out = subprocess.run([sys.executable, "-c", M4RM_GEOM_CASE % {"root": root}], env=env,
+                         cwd=root, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.strip().splitlines()[-1] == "BAD []", out.stdout[-2000:]
