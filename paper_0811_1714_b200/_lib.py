@@ -135,13 +135,25 @@ def check(rc: int) -> None:
     raise DeviceError(f"native error {rc}: {msg}")
 
 
+def _raw_stream_fn():
+    import torch
+    c = torch._C
+    if hasattr(c, "_cuda_getCurrentRawStream") and hasattr(c, "_cuda_getDevice"):
+        return lambda: c._cuda_getCurrentRawStream(c._cuda_getDevice())
+    return lambda: torch.cuda.current_stream().cuda_stream  # public API fallback
+
+
+_raw_stream = None
+
+
 def current_stream() -> int:
     """Raw cudaStream_t of torch's current stream on the current device
     (the same value as torch.cuda.current_stream().cuda_stream, without
     building a Stream object: ~0.3 us instead of ~3.5 us per call)."""
-    import torch
-    c = torch._C
-    return c._cuda_getCurrentRawStream(c._cuda_getDevice())
+    global _raw_stream
+    if _raw_stream is None:
+        _raw_stream = _raw_stream_fn()
+    return _raw_stream()
 
 
 def launch_count() -> int:

@@ -64,7 +64,7 @@ class BitMatrix:
         self.width = words_per_row(ncols)
         self.pitch = int(lib.gf2_pitch_words(ncols))
         if device is None:
-            device = torch._C._cuda_getDevice()  # index on the current device
+            device = torch.cuda.current_device()  # index on the current device
         if _overwritten and self.pitch == self.width and ncols % 64 == 0:
             # a product target whose every word the kernels overwrite whole
             # (no padding words, no partial last word to merge into): no fill
