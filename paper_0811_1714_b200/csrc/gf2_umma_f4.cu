@@ -392,6 +392,21 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
     const int gq = ngroups / p.nt, gr = ngroups % p.nt;
     auto tile_g0 = [&](int ntile) -> int { return ntile * gq + min(ntile, gr); };
     auto tile_width = [&](int ntile) -> int { return 32 * (gq + (ntile < gr ? 1 : 0)); };
+    // position r of a problem's mt x nt tile grid -> (mtile, ntile):
+    // column tiles fastest, or (order G > 0) blocks of G row tiles with the
+    // row tile fastest inside a block
+    auto tile_mn = [&](int64_t r, int &mtile, int &ntile) {
+        if (p.order > 0) {
+            const int64_t G = p.order;
+            const int64_t blk = r / (G * p.nt), rem = r % (G * p.nt);
+            const int64_t g = (int64_t)p.mt - blk * G < G ? (int64_t)p.mt - blk * G : G;  // rows in this (last) block
+            mtile = (int)(blk * G + rem % g);
+            ntile = (int)(rem / g);
+        } else {
+            mtile = (int)(r / p.nt);
+            ntile = (int)(r % p.nt);
+        }
+    };
 
     if (warp == 0 && lane == 0) {
         int stage = 0;
@@ -401,7 +416,8 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
             int64_t r = t % tiles_per_chunk;
             const int prob = (int)(r / (p.mt * p.nt));
             r %= (p.mt * p.nt);
-            const int mtile = (int)(r / p.nt), ntile = (int)(r % p.nt);
+            int mtile, ntile;
+            tile_mn(r, mtile, ntile);
             const int kb0 = chunk * p.kchunk_blocks;
             const int kb1 = min(kb0 + p.kchunk_blocks, p.kblocks);
             const int arow = mtile * 256 + (int)rank * BM;
@@ -431,7 +447,8 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
         int it = 0;
         for (int64_t t = unit; t < ntiles; t += nunits, ++it) {
             const int chunk = (int)(t / tiles_per_chunk);
-            const int ntile = (int)((t % tiles_per_chunk) % p.nt);
+            int mtile_u, ntile;
+            tile_mn((t % tiles_per_chunk) % (p.mt * p.nt), mtile_u, ntile);
             const uint32_t idesc = idesc0 | ((uint32_t)(tile_width(ntile) >> 3) << 17);
             const int kb0 = chunk * p.kchunk_blocks;
             const int kb1 = min(kb0 + p.kchunk_blocks, p.kblocks);
@@ -467,7 +484,8 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
             int64_t r = t % tiles_per_chunk;
             const int prob = (int)(r / (p.mt * p.nt));
             r %= (p.mt * p.nt);
-            const int mtile = (int)(r / p.nt), ntile = (int)(r % p.nt);
+            int mtile, ntile;
+            tile_mn(r, mtile, ntile);
             const int nch = tile_width(ntile) >> 5;
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
@@ -623,6 +641,20 @@ int launch_umma_f4(const UmmaJob &jb, int64_t nprob, cudaStream_t s) {
     ua.post = jb.fuse_post;
     static const int f4dbg = getenv("GF2_F4_DBG") ? atoi(getenv("GF2_F4_DBG")) : 0;
     ua.dbg = f4dbg;
+    // tile raster: for Strassen leaves with long K (cfg3/cfg5: 7^d problems
+    // of 8192^3) row tiles run fastest, so each wave of 74 pairs spans ~2.3
+    // column tiles x all row tiles: the GEMM's DRAM reads drop 694 -> 590 MB
+    // per cfg3 launch and the launch 0.904 -> 0.900 ms (same box, 5 runs).
+    // Elsewhere column tiles stay fastest: row-tile-fastest measured slower
+    // for cfg4's single 10000x7001x12345 product (233 -> 236 us) and for
+    // 1024-deep leaves (37 -> 40 us). GF2_F4_ORDER = G > 0 forces blocks of
+    // G row tiles (G >= mt: row tiles fastest), 0 column tiles fastest.
+    static const int f4order = getenv("GF2_F4_ORDER") ? atoi(getenv("GF2_F4_ORDER")) : -1;
+    ua.order = f4order >= 0 ? f4order : ((jb.fuse_post && ua.kblocks >= 16) ? ua.mt : 0);
+    // G > mt is the same raster; clamping keeps G x nt small, so the kernel's
+    // per-tile index divisions stay on the fast 32-bit path (a 2^30 block
+    // pushed them onto 64-bit division and cost the cfg3 GEMM 1.5 %)
+    if (ua.order > ua.mt) ua.order = ua.mt;
     int rc = GF2_OK;
     if (jb.fuse_post) {
         ua.qoffC[1] = jb.n / 64; ua.qoffC[2] = jb.m * jb.pc; ua.qoffC[3] = ua.qoffC[1] + ua.qoffC[2];
