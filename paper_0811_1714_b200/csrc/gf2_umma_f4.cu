@@ -204,6 +204,31 @@ __global__ void __launch_bounds__(256) k_expand4_cols(ExpandArgs a) {
     }
 }
 
+// 32 f32 accumulators (integer sums < 2^23) -> their parities packed
+// MSB-first (bit 31 - j = parity of column j). Adding 2^23 puts each sum's
+// integer value in the mantissa, so bit 0 is the parity (FADD2: two columns
+// per instruction). The low bytes of 4 columns j = k, 8+k, 16+k, 24+k are
+// gathered into one word with two-level byte permutes (3 PRMT); the 8 words
+// k = 0..7 then go to bit 7 - k of every byte with one shift and one masked
+// OR each: 56 instructions per 32 columns instead of 96.
+__device__ __forceinline__ uint32_t parity_pack32(const uint32_t *v) {
+    uint32_t u[32];
+#pragma unroll
+    for (int j = 0; j < 32; j += 2)
+        asm("{\n.reg .b64 a, r;\nmov.b64 a, {%2, %3};\nadd.rn.f32x2 r, a, %4;\nmov.b64 {%0, %1}, r;\n}\n"
+            : "=r"(u[j]), "=r"(u[j + 1])
+            : "r"(v[j]), "r"(v[j + 1]), "l"(0x4B0000004B000000ULL));
+    uint32_t pk = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t hi = __byte_perm(u[24 + k], u[16 + k], 0x0040);  // bytes: u[24+k].b0, u[16+k].b0
+        const uint32_t lo = __byte_perm(u[8 + k], u[k], 0x0040);        // bytes: u[8+k].b0, u[k].b0
+        const uint32_t t = __byte_perm(hi, lo, 0x5410);                 // [u24+k, u16+k, u8+k, uk]
+        pk |= (t << (7 - k)) & (0x01010101u << (7 - k));
+    }
+    return pk;
+}
+
 __device__ __forceinline__ void umma_f4(uint32_t taddr, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc,
                                         uint32_t sfa, uint32_t sfb) {
     asm volatile(
@@ -512,14 +537,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
                 packed[c] = 0;
                 if (c < nch) {
                     if (c + 1 < nch) TMEM_LD32(trow + (c + 1) * 32, vb[(c + 1) & 1]);
-                    const uint32_t *v = vb[c & 1];
-                    uint32_t part[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const uint32_t u = __float_as_uint(__uint_as_float(v[j]) + 8388608.0f);
-                        part[j & 3] |= (u << (31 - j)) & (1u << (31 - j));
-                    }
-                    packed[c] = (part[0] | part[1]) | (part[2] | part[3]);
+                    packed[c] = parity_pack32(vb[c & 1]);
                     if (c + 1 < nch) TMEM_WAIT_LD32(vb[(c + 1) & 1]);
                 }
             }
