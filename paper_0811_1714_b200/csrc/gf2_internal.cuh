@@ -60,6 +60,68 @@ int check_cuda(cudaError_t e, const char *what);
 extern std::atomic<int64_t> g_launches;
 inline void note_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// Programmatic dependent launch (PDL). Every library kernel is launched
+// with programmatic stream serialization and executes griddepcontrol.wait
+// before its first global memory access (the tensor-core GEMMs after their
+// barrier/TMEM/scale-factor setup): the next kernel of the stream is
+// dispatched as the previous one's CTAs exit, instead of after its
+// completion has been signalled back, and waits for its memory. Ordering is
+// exactly stream order. No kernel triggers its dependents early
+// (GF2_PDL_TRIGGER=0, measured best: an early trigger let waiting CTAs
+// crowd the primaries -- 4096^3 45.3 us with no trigger, 51.4 with a
+// trigger at every kernel's start, 49.4 without PDL; 3000^3 at cutoff 512
+// 109 / 113 / 142 us). GF2_PDL=0 turns the attribute off.
+#ifndef GF2_PDL_TRIGGER
+#define GF2_PDL_TRIGGER 0  // 0: implicit trigger at exit; 1: every kernel triggers at its start; 2: not the GEMMs
+#endif
+__device__ __forceinline__ void pdl_trigger() {
+    if (GF2_PDL_TRIGGER == 1) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+__device__ __forceinline__ void pdl_trigger_light() {  // kernels other than the persistent GEMMs
+    if (GF2_PDL_TRIGGER >= 1) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_begin() {
+    pdl_trigger_light();
+    pdl_wait();
+}
+inline int pdl_enabled() {
+    static const int on = getenv("GF2_PDL") ? atoi(getenv("GF2_PDL")) : 1;
+    return on;
+}
+// kernel<<<grid, block, smem, s>>>(args...) with the PDL attribute (and an
+// optional cluster shape); returns the launch error.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            int cluster_x, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    ++na;
+    if (cluster_x > 1) {
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = (unsigned)cluster_x;
+        at[na].val.clusterDim.y = 1;
+        at[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+#define GF2_LAUNCH(...)                                                          \
+    do {                                                                         \
+        cudaError_t _le = (__VA_ARGS__);                                         \
+        if (_le != cudaSuccess) return check_cuda(_le, "kernel launch");         \
+    } while (0)
+
 #define GF2_TRY(expr)                  \
     do {                               \
         int _rc = (expr);              \

@@ -30,6 +30,7 @@ __device__ __forceinline__ void put_word(u64 *p, int64_t j, int64_t last, u64 tm
 // core.py:191-208 -- word (r, j) = splitmix over flat index (row_base+r)*width+j.
 __global__ void k_random(u64 *data, int64_t pitch, int64_t nrows, int64_t width, u64 tm,
                          u64 seed, int64_t row_base) {
+    pdl_begin();
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= width) return;
     for (int64_t r = (int64_t)blockIdx.y * blockDim.y + threadIdx.y; r < nrows;
@@ -43,6 +44,7 @@ __global__ void k_random(u64 *data, int64_t pitch, int64_t nrows, int64_t width,
 // bit (r, c) = [splitmix(seed + (e+1)*golden) < T], e = (row_base+r)*ncols + c.
 __global__ void k_bernoulli(u64 *data, int64_t pitch, int64_t nrows, int64_t ncols, int64_t width,
                             u64 tm, u64 seed, u64 thresh, int64_t row_base) {
+    pdl_begin();
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= width) return;
     for (int64_t r = (int64_t)blockIdx.y * blockDim.y + threadIdx.y; r < nrows;
@@ -65,6 +67,7 @@ __global__ void k_bernoulli(u64 *data, int64_t pitch, int64_t nrows, int64_t nco
 template <int OP>
 __global__ void k_ewise(u64 *out, int64_t po, const u64 *a, int64_t pa, const u64 *b, int64_t pb,
                         int64_t nrows, int64_t width, u64 tm) {
+    pdl_begin();
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= width) return;
     for (int64_t r = (int64_t)blockIdx.y * blockDim.y + threadIdx.y; r < nrows;
@@ -80,6 +83,7 @@ __global__ void k_ewise(u64 *out, int64_t po, const u64 *a, int64_t pa, const u6
 // aligned), ROWS rows per thread with all loads issued before the stores.
 template <int VEC, int ROWS>
 __global__ void k_combine(CombineArgs p, int64_t wblocks) {
+    pdl_begin();
     typedef typename std::conditional<VEC == 2, ulonglong2, unsigned long long>::type V;
     const int64_t o = blockIdx.x / wblocks;
     const int64_t j = ((blockIdx.x % wblocks) * blockDim.x + threadIdx.x) * VEC;
@@ -149,6 +153,7 @@ __global__ void k_combine(CombineArgs p, int64_t wblocks) {
 // Same CombineArgs addressing; 16-byte vectors, ROWS rows per thread.
 template <int NS, int NQ, int ROWS>
 __global__ void k_combine_all(CombineArgs p, int64_t wblocks) {
+    pdl_begin();
     const int64_t prob = blockIdx.x / wblocks;
     const int64_t j = ((blockIdx.x % wblocks) * blockDim.x + threadIdx.x) * 2;
     if (j >= p.W) return;
@@ -194,6 +199,7 @@ __global__ void k_combine_all(CombineArgs p, int64_t wblocks) {
 constexpr int CT_ROWS = 256, CT_WORDS = 8;
 constexpr int CT_SMEM = 4 * CT_ROWS * (CT_WORDS + 1) * 8;
 __global__ void __launch_bounds__(256) k_combine_t(CombineArgs p) {
+    pdl_begin();
     extern __shared__ __align__(16) unsigned char ct_smem[];
     u64(*tile)[CT_ROWS][CT_WORDS + 1] = reinterpret_cast<u64(*)[CT_ROWS][CT_WORDS + 1]>(ct_smem);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -286,8 +292,8 @@ int launch_random(const gf2_view &v, u64 seed, int64_t row_base, cudaStream_t s)
     int64_t width = words_per_row(v.ncols);
     if (!width || !v.nrows) return GF2_OK;
     dim3 blk = row_block(width);
-    k_random<<<row_grid(width, v.nrows, blk), blk, 0, s>>>(v.data, v.pitch, v.nrows, width,
-                                                         tail_mask(v.ncols), seed, row_base);
+    GF2_LAUNCH(launch_k(k_random, row_grid(width, v.nrows, blk), blk, 0, s, 1, v.data, v.pitch, v.nrows, width,
+                                                         tail_mask(v.ncols), seed, row_base));
     note_launch();
     return check_cuda(cudaGetLastError(), "k_random launch");
 }
@@ -296,8 +302,8 @@ int launch_bernoulli(const gf2_view &v, u64 seed, u64 thresh, int64_t row_base, 
     int64_t width = words_per_row(v.ncols);
     if (!width || !v.nrows) return GF2_OK;
     dim3 blk = row_block(width);
-    k_bernoulli<<<row_grid(width, v.nrows, blk), blk, 0, s>>>(
-        v.data, v.pitch, v.nrows, v.ncols, width, tail_mask(v.ncols), seed, thresh, row_base);
+    GF2_LAUNCH(launch_k(k_bernoulli, row_grid(width, v.nrows, blk), blk, 0, s, 1, 
+        v.data, v.pitch, v.nrows, v.ncols, width, tail_mask(v.ncols), seed, thresh, row_base));
     note_launch();
     return check_cuda(cudaGetLastError(), "k_bernoulli launch");
 }
@@ -309,13 +315,13 @@ int launch_ewise(const gf2_view &out, const gf2_view *a, const gf2_view *b, int 
     dim3 grd = row_grid(width, out.nrows, blk);
     u64 tm = tail_mask(out.ncols);
     if (op == 0)
-        k_ewise<0><<<grd, blk, 0, s>>>(out.data, out.pitch, nullptr, 0, nullptr, 0, out.nrows, width, tm);
+        GF2_LAUNCH(launch_k(k_ewise<0>, grd, blk, 0, s, 1, out.data, out.pitch, nullptr, 0, nullptr, 0, out.nrows, width, tm));
     else if (op == 1)
-        k_ewise<1><<<grd, blk, 0, s>>>(out.data, out.pitch, a->data, a->pitch, nullptr, 0, out.nrows,
-                                       width, tm);
+        GF2_LAUNCH(launch_k(k_ewise<1>, grd, blk, 0, s, 1, out.data, out.pitch, a->data, a->pitch, nullptr, 0, out.nrows,
+                                       width, tm));
     else
-        k_ewise<2><<<grd, blk, 0, s>>>(out.data, out.pitch, a->data, a->pitch, b->data, b->pitch,
-                                       out.nrows, width, tm);
+        GF2_LAUNCH(launch_k(k_ewise<2>, grd, blk, 0, s, 1, out.data, out.pitch, a->data, a->pitch, b->data, b->pitch,
+                                       out.nrows, width, tm));
     note_launch();
     return check_cuda(cudaGetLastError(), "k_ewise launch");
 }
@@ -350,19 +356,19 @@ int launch_combine(const CombineArgs &a, cudaStream_t s) {
     unsigned used = 0;
     for (int q = 0; q < a.nq; ++q) used |= a.mask[q];
     if (v2 && a.nq == 7 && used == 0xF) {
-        k_combine_all<4, 7, 2><<<dim3((unsigned)(wblocks * a.nprob), (unsigned)gy2, 1), blk, 0, s>>>(a, wblocks);
+        GF2_LAUNCH(launch_k(k_combine_all<4, 7, 2>, dim3((unsigned)(wblocks * a.nprob), (unsigned)gy2, 1), blk, 0, s, 1, a, wblocks));
         note_launch();
         return check_cuda(cudaGetLastError(), "k_combine_all launch");
     }
     if (v2 && a.nq == 4 && used == 0x7F) {
-        k_combine_all<7, 4, 2><<<dim3((unsigned)(wblocks * a.nprob), (unsigned)gy2, 1), blk, 0, s>>>(a, wblocks);
+        GF2_LAUNCH(launch_k(k_combine_all<7, 4, 2>, dim3((unsigned)(wblocks * a.nprob), (unsigned)gy2, 1), blk, 0, s, 1, a, wblocks));
         note_launch();
         return check_cuda(cudaGetLastError(), "k_combine_all launch");
     }
     if (v2)
-        k_combine<2, ROWS><<<dim3((unsigned)gx, (unsigned)gy, 1), blk, 0, s>>>(a, wblocks);
+        GF2_LAUNCH(launch_k(k_combine<2, ROWS>, dim3((unsigned)gx, (unsigned)gy, 1), blk, 0, s, 1, a, wblocks));
     else
-        k_combine<1, ROWS><<<dim3((unsigned)gx, (unsigned)gy, 1), blk, 0, s>>>(a, wblocks);
+        GF2_LAUNCH(launch_k(k_combine<1, ROWS>, dim3((unsigned)gx, (unsigned)gy, 1), blk, 0, s, 1, a, wblocks));
     note_launch();
     return check_cuda(cudaGetLastError(), "k_combine launch");
 }
@@ -382,7 +388,7 @@ int launch_combine_t(const CombineArgs &a, cudaStream_t s) {
         GF2_TRY(check_cuda(cudaFuncSetAttribute(k_combine_t, cudaFuncAttributeMaxDynamicSharedMemorySize, CT_SMEM),
                            "combine_t smem attr"));
     dim3 grd((unsigned)((a.W + CT_WORDS - 1) / CT_WORDS), (unsigned)((a.R + CT_ROWS - 1) / CT_ROWS), (unsigned)a.nprob);
-    k_combine_t<<<grd, 256, CT_SMEM, s>>>(a);
+    GF2_LAUNCH(launch_k(k_combine_t, grd, 256, CT_SMEM, s, 1, a));
     note_launch();
     return check_cuda(cudaGetLastError(), "k_combine_t launch");
 }

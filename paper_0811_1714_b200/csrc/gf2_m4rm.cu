@@ -134,6 +134,7 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
 template <int RPT, bool TMA>
 __global__ void __launch_bounds__(kThreads, 1)
     k_m4rm(KArgs p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
+    pdl_begin();
     constexpr int BM = kRowGroups * RPT;
     constexpr int kABox = a_box_rows<RPT>();
     extern __shared__ __align__(128) unsigned char smem[];
@@ -314,7 +315,7 @@ int launch_rpt(const KArgs &ka, const CUtensorMap &ta, const CUtensorMap &tb, in
         GF2_TRY(check_cuda(cudaFuncSetAttribute(k_m4rm<RPT, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
                            "cudaFuncSetAttribute(k_m4rm)"));
     dim3 grid((unsigned)col_tiles, (unsigned)row_tiles, (unsigned)zdim);
-    k_m4rm<RPT, TMA><<<grid, kThreads, sm, s>>>(ka, ta, tb);
+    GF2_LAUNCH(launch_k(k_m4rm<RPT, TMA>, grid, kThreads, sm, s, 1, ka, ta, tb));
     note_launch();
     return check_cuda(cudaGetLastError(), "k_m4rm launch");
 }

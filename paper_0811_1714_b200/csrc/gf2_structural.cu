@@ -21,6 +21,7 @@ namespace {
 constexpr int TR_ROWS = 512, TR_WORDS = 4, TR_OUT_WORDS = TR_ROWS / 64;
 __global__ void __launch_bounds__(256) k_transpose(const u64 *__restrict__ in, int64_t pin, u64 *__restrict__ out,
                                                    int64_t pout, int64_t rows, int64_t cols) {
+    pdl_begin();
     __shared__ u64 tile[TR_ROWS][TR_WORDS + 1];
     __shared__ u64 stg[64 * TR_WORDS][TR_OUT_WORDS + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -70,6 +71,7 @@ __global__ void __launch_bounds__(256) k_transpose(const u64 *__restrict__ in, i
 // Narrow-B cubic product: one thread per (row i, output word); BT is B^T.
 __global__ void k_cubic(const u64 *__restrict__ A, int64_t pa, const u64 *__restrict__ BT, int64_t pbt,
                         u64 *__restrict__ C, int64_t pc, int64_t m, int64_t l, int64_t n, int accumulate) {
+    pdl_begin();
     const int64_t Wn = words_per_row(n), Wl = words_per_row(l);
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= m * Wn) return;
@@ -99,6 +101,7 @@ __global__ void k_cubic(const u64 *__restrict__ A, int64_t pa, const u64 *__rest
 // dst[:, c0:c0+n) = src[:, 0:n), any c0; one thread per destination word.
 __global__ void k_copy_cols(const u64 *__restrict__ src, int64_t ps, u64 *__restrict__ dst, int64_t pd,
                             int64_t rows, int64_t c0, int64_t n) {
+    pdl_begin();
     const int64_t w0 = c0 / 64, w1 = (c0 + n - 1) / 64;  // destination words touched
     const int64_t nw = w1 - w0 + 1;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -130,7 +133,7 @@ int launch_transpose(const gf2_view &out, const gf2_view &in, cudaStream_t s) {
     const int64_t wcols = words_per_row(in.ncols);
     if (!wcols || !in.nrows) return GF2_OK;
     dim3 grd((unsigned)((wcols + TR_WORDS - 1) / TR_WORDS), (unsigned)((in.nrows + TR_ROWS - 1) / TR_ROWS));
-    k_transpose<<<grd, 256, 0, s>>>(in.data, in.pitch, out.data, out.pitch, in.nrows, in.ncols);
+    GF2_LAUNCH(launch_k(k_transpose, grd, 256, 0, s, 1, in.data, in.pitch, out.data, out.pitch, in.nrows, in.ncols));
     note_launch();
     return check_cuda(cudaGetLastError(), "k_transpose launch");
 }
@@ -138,8 +141,8 @@ int launch_transpose(const gf2_view &out, const gf2_view &in, cudaStream_t s) {
 int launch_cubic(const gf2_view &c, const gf2_view &a, const gf2_view &bt, int accumulate, cudaStream_t s) {
     const int64_t work = c.nrows * words_per_row(c.ncols);
     if (!work) return GF2_OK;
-    k_cubic<<<(unsigned)((work + 127) / 128), 128, 0, s>>>(a.data, a.pitch, bt.data, bt.pitch, c.data, c.pitch,
-                                                           a.nrows, a.ncols, c.ncols, accumulate);
+    GF2_LAUNCH(launch_k(k_cubic, (unsigned)((work + 127) / 128), 128, 0, s, 1, a.data, a.pitch, bt.data, bt.pitch, c.data, c.pitch,
+                                                           a.nrows, a.ncols, c.ncols, accumulate));
     note_launch();
     return check_cuda(cudaGetLastError(), "k_cubic launch");
 }
@@ -148,8 +151,8 @@ int launch_copy_cols(const gf2_view &dst, int64_t c0, const gf2_view &src, cudaS
     if (!src.nrows || !src.ncols) return GF2_OK;
     const int64_t nw = (c0 + src.ncols - 1) / 64 - c0 / 64 + 1;
     const int64_t work = src.nrows * nw;
-    k_copy_cols<<<(unsigned)((work + 255) / 256), 256, 0, s>>>(src.data, src.pitch, dst.data, dst.pitch, src.nrows,
-                                                               c0, src.ncols);
+    GF2_LAUNCH(launch_k(k_copy_cols, (unsigned)((work + 255) / 256), 256, 0, s, 1, src.data, src.pitch, dst.data, dst.pitch, src.nrows,
+                                                               c0, src.ncols));
     note_launch();
     return check_cuda(cudaGetLastError(), "k_copy_cols launch");
 }

@@ -52,6 +52,7 @@ __device__ __forceinline__ void expand_store(const ExpandArgs &a, uint8_t *drow,
 
 template <int LEVELS>
 __global__ void k_expand(ExpandArgs a) {
+    pdl_begin();
     const int64_t width = words_per_row(a.cols);
     const int lane = threadIdx.x & 31;
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -127,6 +128,7 @@ struct Geo {
 template <int KIND, int CG>
 __global__ void __launch_bounds__(UMMA_THREADS, 1)
     k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, UArgs p) {
+    pdl_trigger();
     using G = Geo<CG>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;  // 128-byte swizzle atoms
@@ -174,6 +176,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
         cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder_ptr;
+    pdl_wait();  // setup above overlapped the previous kernel's tail
 
     const int64_t tiles_per_chunk = p.nprob * p.mt * p.nt;
     const int64_t ntiles = tiles_per_chunk * p.nchunks;
@@ -359,6 +362,7 @@ constexpr int CV_SMEM = CV_STG * (CV_A_ST + CV_B_ST) + CV_PST * CV_P_ST + 2048;
 static_assert(CV_SMEM <= 232448, "k_umma_cv shared memory");
 
 __global__ void __launch_bounds__(CV_THREADS, 1) k_umma_cv(CvArgs cv, UArgs p) {
+    pdl_trigger();
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     const uint32_t sA = base_u32;
@@ -396,6 +400,7 @@ __global__ void __launch_bounds__(CV_THREADS, 1) k_umma_cv(CvArgs cv, UArgs p) {
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder_ptr;
+    pdl_wait();  // setup above overlapped the previous kernel's tail
 
     const int64_t tiles = p.nprob * p.mt * p.nt;
 
@@ -683,11 +688,11 @@ int launch_expand(const ExpandArgs &a, int64_t nprob, cudaStream_t s) {
     dim3 grd((unsigned)((width + blk.x - 1) / blk.x), (unsigned)std::min<int64_t>(65535, (a.rows + 1) / 2),
              (unsigned)nprob);
     if (a.levels == 0)
-        k_expand<0><<<grd, blk, 0, s>>>(a);
+        GF2_LAUNCH(launch_k(k_expand<0>, grd, blk, 0, s, 1, a));
     else if (a.levels == 1)
-        k_expand<1><<<grd, blk, 0, s>>>(a);
+        GF2_LAUNCH(launch_k(k_expand<1>, grd, blk, 0, s, 1, a));
     else
-        k_expand<2><<<grd, blk, 0, s>>>(a);
+        GF2_LAUNCH(launch_k(k_expand<2>, grd, blk, 0, s, 1, a));
     note_launch();
     return check_cuda(cudaGetLastError(), "k_expand launch");
 }
@@ -776,20 +781,9 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
         }
         const int64_t tiles = nprob * ua.mt * ua.nt;
         const int64_t pairs = std::min<int64_t>(tiles, num_sms() / 2);
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3((unsigned)(2 * pairs));
-        cfg.blockDim = dim3(CV_THREADS);
-        cfg.dynamicSmemBytes = CV_SMEM;
-        cfg.stream = s;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
         const int tidx = timer_begin(s, (double)jb.m * (double)jb.l * (double)jb.n * (double)nprob);
-        int rc = check_cuda(cudaLaunchKernelEx(&cfg, k_umma_cv, cv, ua), "k_umma_cv launch");
+        int rc = check_cuda(launch_k(k_umma_cv, dim3((unsigned)(2 * pairs)), dim3(CV_THREADS), CV_SMEM, s, 2, cv, ua),
+                            "k_umma_cv launch");
         note_launch();
         timer_end(tidx, s);
         return rc;
@@ -874,27 +868,16 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
         if (cg == 1) {
             const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
             if (kind == 0)
-                k_umma<0, 1><<<grid, UMMA_THREADS, Geo<1>::SMEM, s>>>(ta, tb, ua);
+                GF2_LAUNCH(launch_k(k_umma<0, 1>, grid, UMMA_THREADS, Geo<1>::SMEM, s, 1, ta, tb, ua));
             else
-                k_umma<1, 1><<<grid, UMMA_THREADS, Geo<1>::SMEM, s>>>(ta, tb, ua);
+                GF2_LAUNCH(launch_k(k_umma<1, 1>, grid, UMMA_THREADS, Geo<1>::SMEM, s, 1, ta, tb, ua));
         } else {
             const int64_t pairs = std::min<int64_t>(ntiles, num_sms() / 2);
-            cudaLaunchConfig_t cfg{};
-            cfg.gridDim = dim3((unsigned)(2 * pairs));
-            cfg.blockDim = dim3(UMMA_THREADS);
-            cfg.dynamicSmemBytes = Geo<2>::SMEM;
-            cfg.stream = s;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = 2;
-            attr[0].val.clusterDim.y = 1;
-            attr[0].val.clusterDim.z = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
+            const dim3 g2((unsigned)(2 * pairs)), b2(UMMA_THREADS);
             if (kind == 0)
-                rc = check_cuda(cudaLaunchKernelEx(&cfg, k_umma<0, 2>, ta, tb, ua), "k_umma 2sm launch");
+                rc = check_cuda(launch_k(k_umma<0, 2>, g2, b2, Geo<2>::SMEM, s, 2, ta, tb, ua), "k_umma 2sm launch");
             else
-                rc = check_cuda(cudaLaunchKernelEx(&cfg, k_umma<1, 2>, ta, tb, ua), "k_umma 2sm launch");
+                rc = check_cuda(launch_k(k_umma<1, 2>, g2, b2, Geo<2>::SMEM, s, 2, ta, tb, ua), "k_umma 2sm launch");
         }
         note_launch();
         if (rc == GF2_OK) rc = check_cuda(cudaGetLastError(), "k_umma launch");

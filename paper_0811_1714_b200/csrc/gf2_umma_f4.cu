@@ -54,6 +54,7 @@ __device__ __forceinline__ uint32_t nib_word(u64 v, int t) {
 constexpr int F4_ROWS_PER_WARP = 4;
 template <int LEVELS>
 __global__ void __launch_bounds__(256) k_expand4_rows(ExpandArgs a) {
+    pdl_begin();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t width = words_per_row(a.cols);
     const int64_t j0 = (int64_t)blockIdx.x * 32, j = j0 + lane;
@@ -93,6 +94,7 @@ __global__ void __launch_bounds__(256) k_expand4_rows(ExpandArgs a) {
 // times per 7 outputs.
 template <int ROWS>
 __global__ void __launch_bounds__(256) k_expand4_rows7(ExpandArgs a) {
+    pdl_begin();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t width = words_per_row(a.cols);
     const int64_t j0 = (int64_t)blockIdx.x * 32, j = j0 + lane;
@@ -145,6 +147,7 @@ constexpr int F4T_TILE_BYTES = F4T_ROWS * (F4T_WORDS + 1) * 8;
 constexpr int F4T_SMEM = F4T_TILE_BYTES + 8 * 32 * F4T_STG_PITCH;
 template <int LEVELS>
 __global__ void __launch_bounds__(256) k_expand4_cols(ExpandArgs a) {
+    pdl_begin();
     extern __shared__ __align__(16) unsigned char f4t_smem[];
     u64(*tile)[F4T_WORDS + 1] = reinterpret_cast<u64(*)[F4T_WORDS + 1]>(f4t_smem);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -380,6 +383,7 @@ __device__ __forceinline__ void xor_rows_f4(const UArgs &p, const uint32_t *pack
 // (all 0x7F) at 448..511 in both CTAs.
 __global__ void __launch_bounds__(UMMA_THREADS, 1)
     k_umma_f4(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, UArgs p) {
+    pdl_trigger();
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     const uint32_t sA = base_u32;
@@ -429,6 +433,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
     tc_fence_before();
     cluster_sync();
     tc_fence_after();
+    pdl_wait();  // barrier init, TMEM alloc and scale factors overlapped the previous kernel's tail
 
     const int64_t tiles_per_chunk = p.nprob * p.mt * p.nt;
     const int64_t ntiles = tiles_per_chunk * p.nchunks;
@@ -598,7 +603,7 @@ static int launch_expand4(const ExpandArgs &a, int64_t nprob, bool cols, cudaStr
         // 2 rows per warp: 48 registers, more resident blocks and a finer grid
         // than 4 (43 vs 45 us at cfg3; forcing occupancy via launch bounds spills)
         dim3 grd((unsigned)((width + 31) / 32), (unsigned)((a.rows + 8 * 2 - 1) / (8 * 2)), (unsigned)(nprob / 7));
-        k_expand4_rows7<2><<<grd, 256, 0, s>>>(a);
+        GF2_LAUNCH(launch_k(k_expand4_rows7<2>, grd, 256, 0, s, 1, a));
         note_launch();
         return check_cuda(cudaGetLastError(), "k_expand4_rows7 launch");
     }
@@ -606,11 +611,11 @@ static int launch_expand4(const ExpandArgs &a, int64_t nprob, bool cols, cudaStr
         dim3 grd((unsigned)((width + 31) / 32), (unsigned)((a.rows + 8 * F4_ROWS_PER_WARP - 1) / (8 * F4_ROWS_PER_WARP)),
                  (unsigned)nprob);
         if (a.levels == 0)
-            k_expand4_rows<0><<<grd, 256, 0, s>>>(a);
+            GF2_LAUNCH(launch_k(k_expand4_rows<0>, grd, 256, 0, s, 1, a));
         else if (a.levels == 1)
-            k_expand4_rows<1><<<grd, 256, 0, s>>>(a);
+            GF2_LAUNCH(launch_k(k_expand4_rows<1>, grd, 256, 0, s, 1, a));
         else
-            k_expand4_rows<2><<<grd, 256, 0, s>>>(a);
+            GF2_LAUNCH(launch_k(k_expand4_rows<2>, grd, 256, 0, s, 1, a));
     } else {
         // a.dp = bytes per K-major row = (K rows rounded to 64) / 2
         dim3 grd((unsigned)((width + F4T_WORDS - 1) / F4T_WORDS), (unsigned)((a.dp * 2 + F4T_ROWS - 1) / F4T_ROWS),
@@ -625,11 +630,11 @@ static int launch_expand4(const ExpandArgs &a, int64_t nprob, bool cols, cudaStr
                                                     F4T_SMEM), "expand4 smem attr"));
         }
         if (a.levels == 0)
-            k_expand4_cols<0><<<grd, 256, F4T_SMEM, s>>>(a);
+            GF2_LAUNCH(launch_k(k_expand4_cols<0>, grd, 256, F4T_SMEM, s, 1, a));
         else if (a.levels == 1)
-            k_expand4_cols<1><<<grd, 256, F4T_SMEM, s>>>(a);
+            GF2_LAUNCH(launch_k(k_expand4_cols<1>, grd, 256, F4T_SMEM, s, 1, a));
         else
-            k_expand4_cols<2><<<grd, 256, F4T_SMEM, s>>>(a);
+            GF2_LAUNCH(launch_k(k_expand4_cols<2>, grd, 256, F4T_SMEM, s, 1, a));
     }
     note_launch();
     return check_cuda(cudaGetLastError(), "k_expand4 launch");
@@ -744,20 +749,9 @@ int launch_umma_f4(const UmmaJob &jb, int64_t nprob, cudaStream_t s) {
         if (rc != GF2_OK) break;
         const int64_t ntiles = (int64_t)ua.nchunks * nq * ua.mt * ua.nt;
         const int64_t pairs = std::min<int64_t>(ntiles, num_sms() / 2);
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3((unsigned)(2 * pairs));
-        cfg.blockDim = dim3(UMMA_THREADS);
-        cfg.dynamicSmemBytes = F4_SMEM;
-        cfg.stream = s;
-        cudaLaunchAttribute la[1];
-        la[0].id = cudaLaunchAttributeClusterDimension;
-        la[0].val.clusterDim.x = 2;
-        la[0].val.clusterDim.y = 1;
-        la[0].val.clusterDim.z = 1;
-        cfg.attrs = la;
-        cfg.numAttrs = 1;
         const int tidx = timer_begin(s, (double)jb.m * (double)jb.l * (double)jb.n * (double)nq);
-        rc = check_cuda(cudaLaunchKernelEx(&cfg, k_umma_f4, ta, tb, ua), "k_umma_f4 launch");
+        rc = check_cuda(launch_k(k_umma_f4, dim3((unsigned)(2 * pairs)), dim3(UMMA_THREADS), F4_SMEM, s, 2, ta, tb, ua),
+                        "k_umma_f4 launch");
         note_launch();
         timer_end(tidx, s);
     }
