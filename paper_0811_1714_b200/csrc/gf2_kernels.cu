@@ -151,41 +151,41 @@ __global__ void k_combine(CombineArgs p, int64_t wblocks) {
 // post-additions) and writes all NQ outputs, instead of k_combine's one
 // output per thread re-reading 1-4 sources (14 source reads per 7 outputs).
 // Same CombineArgs addressing; 16-byte vectors, ROWS rows per thread.
-template <int NS, int NQ, int ROWS>
-__global__ void k_combine_all(CombineArgs p, int64_t wblocks) {
+// One row per thread and iteration, __launch_bounds__(256, 3): the earlier
+// 2-row unrolled form took 112 (4 sources) / 139 (7 sources) registers, and
+// the post-addition instance ran one CTA per SM (12 % of warps active) with
+// too few loads in flight for HBM (cfg5: 7->4 levels at 3.9 / 2.8 TB/s).
+template <int NS, int NQ>
+__global__ void __launch_bounds__(256, 3) k_combine_all(CombineArgs p, int64_t wblocks) {
     pdl_begin();
     const int64_t prob = blockIdx.x / wblocks;
     const int64_t j = ((blockIdx.x % wblocks) * blockDim.x + threadIdx.x) * 2;
     if (j >= p.W) return;
     const u64 *sb = p.src + prob * p.src_stride + j;
     u64 *db = p.dst + prob * p.dst_stride + j;
-    const int64_t rstep = (int64_t)gridDim.y * blockDim.y * ROWS;
-    for (int64_t r0 = ((int64_t)blockIdx.y * blockDim.y + threadIdx.y) * ROWS; r0 < p.R; r0 += rstep) {
+    const int64_t rstep = (int64_t)gridDim.y * blockDim.y;
+    for (int64_t r = (int64_t)blockIdx.y * blockDim.y + threadIdx.y; r < p.R; r += rstep) {
+        const u64 *srow = sb + r * p.src_pitch;
+        u64 *drow = db + r * p.dst_pitch;
+        ulonglong2 in[NS];
 #pragma unroll
-        for (int rr = 0; rr < ROWS; ++rr) {
-            const int64_t r = r0 + rr;
-            if (r >= p.R) break;
-            ulonglong2 in[NS];
+        for (int i = 0; i < NS; ++i) in[i] = __ldg(reinterpret_cast<const ulonglong2 *>(srow + p.src_off[i]));
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            ulonglong2 v = make_ulonglong2(0, 0);
 #pragma unroll
             for (int i = 0; i < NS; ++i)
-                in[i] = __ldg(reinterpret_cast<const ulonglong2 *>(sb + p.src_off[i] + r * p.src_pitch));
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                ulonglong2 v = make_ulonglong2(0, 0);
-#pragma unroll
-                for (int i = 0; i < NS; ++i)
-                    if (p.mask[q] & (1u << i)) {
-                        v.x ^= in[i].x;
-                        v.y ^= in[i].y;
-                    }
-                ulonglong2 *d = reinterpret_cast<ulonglong2 *>(db + p.dst_off[q] + r * p.dst_pitch);
-                if (p.accumulate) {
-                    const ulonglong2 o = *d;
-                    v.x ^= o.x;
-                    v.y ^= o.y;
+                if (p.mask[q] & (1u << i)) {
+                    v.x ^= in[i].x;
+                    v.y ^= in[i].y;
                 }
-                *d = v;
+            ulonglong2 *d = reinterpret_cast<ulonglong2 *>(drow + p.dst_off[q]);
+            if (p.accumulate) {
+                const ulonglong2 o = *d;
+                v.x ^= o.x;
+                v.y ^= o.y;
             }
+            *d = v;
         }
     }
 }
@@ -351,17 +351,17 @@ int launch_combine(const CombineArgs &a, cudaStream_t s) {
     const int64_t gx = wblocks * a.nprob * a.nq;
     int64_t gy = (a.R + blk.y * ROWS - 1) / (blk.y * ROWS);
     if (gy > 65535) gy = 65535;
-    int64_t gy2 = (a.R + blk.y * 2 - 1) / (blk.y * 2);
-    if (gy2 > 65535) gy2 = 65535;
+    int64_t gy1 = (a.R + blk.y - 1) / blk.y;
+    if (gy1 > 65535) gy1 = 65535;
     unsigned used = 0;
     for (int q = 0; q < a.nq; ++q) used |= a.mask[q];
     if (v2 && a.nq == 7 && used == 0xF) {
-        GF2_LAUNCH(launch_k(k_combine_all<4, 7, 2>, dim3((unsigned)(wblocks * a.nprob), (unsigned)gy2, 1), blk, 0, s, 1, a, wblocks));
+        GF2_LAUNCH(launch_k(k_combine_all<4, 7>, dim3((unsigned)(wblocks * a.nprob), (unsigned)gy1, 1), blk, 0, s, 1, a, wblocks));
         note_launch();
         return check_cuda(cudaGetLastError(), "k_combine_all launch");
     }
     if (v2 && a.nq == 4 && used == 0x7F) {
-        GF2_LAUNCH(launch_k(k_combine_all<7, 4, 2>, dim3((unsigned)(wblocks * a.nprob), (unsigned)gy2, 1), blk, 0, s, 1, a, wblocks));
+        GF2_LAUNCH(launch_k(k_combine_all<7, 4>, dim3((unsigned)(wblocks * a.nprob), (unsigned)gy1, 1), blk, 0, s, 1, a, wblocks));
         note_launch();
         return check_cuda(cudaGetLastError(), "k_combine_all launch");
     }

@@ -52,6 +52,8 @@ rows = [
     ("lib.gf2_pitch_words", lambda: lib.gf2_pitch_words(1024)),
     ("lib.gf2_version (ctypes floor)", lambda: lib.gf2_version()),
     ("lib.gf2_m4rm(prebuilt views)", lambda: lib.gf2_m4rm(vc, va, vb, 8, 0, s)),
+    ("lib.gf2_add (one ewise launch)", lambda: lib.gf2_add(vc, va, vb, s)),
+    ("lib.gf2_m4rm accumulate (1 launch + maps)", lambda: lib.gf2_m4rm(vc, va, vb, 8, 1, s)),
     ("g.mul_m4rm(a,b,8)", lambda: g.mul_m4rm(a, b, 8)),
     ("lib.gf2_strassen 4096 cutoff 1024", lambda: lib.gf2_strassen(c2._view(), a2._view(), b2._view(), 1024, 8, 0, s)),
     ("g.mul_strassen 4096 cutoff 1024", lambda: g.mul_strassen(a2, b2, p2)),
