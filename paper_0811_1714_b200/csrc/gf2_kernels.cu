@@ -196,9 +196,17 @@ __global__ void __launch_bounds__(256, 3) k_combine_all(CombineArgs p, int64_t w
 // transposes word column w of every quadrant (transpose32, linear, so the
 // XOR commutes with it) and writes each transposed row's 4 words with two
 // 16-byte stores.
-constexpr int CT_ROWS = 256, CT_WORDS = 8;
-constexpr int CT_SMEM = 4 * CT_ROWS * (CT_WORDS + 1) * 8;
+// CT_ROWS = 256 (4 groups of 64 rows, 16-byte output stores); 64-row tiles
+// (one group) when 256-row tiles would leave most SMs idle: cfg2 at cutoff
+// 1024 transposes 2048-row quadrants into 32 tiles of 256 rows.
+constexpr int CT_WORDS = 8;
+template <int CT_ROWS>
+constexpr int ct_smem() {
+    return 4 * CT_ROWS * (CT_WORDS + 1) * 8;
+}
+template <int CT_ROWS>
 __global__ void __launch_bounds__(256) k_combine_t(CombineArgs p) {
+    constexpr int NG = CT_ROWS / 64;
     pdl_begin();
     extern __shared__ __align__(16) unsigned char ct_smem[];
     u64(*tile)[CT_ROWS][CT_WORDS + 1] = reinterpret_cast<u64(*)[CT_ROWS][CT_WORDS + 1]>(ct_smem);
@@ -209,7 +217,7 @@ __global__ void __launch_bounds__(256) k_combine_t(CombineArgs p) {
     // unrolled by 4 kept 4): 652 -> 627 us at cfg5. The kernel is bound by
     // the shuffle transposes' integer work more than by its loads (a version
     // without shared memory, 32 loads in flight per lane, ran 690 us).
-    constexpr int PER = 4 * CT_ROWS * CT_WORDS / 256, BATCH = 16;
+    constexpr int PER = 4 * CT_ROWS * CT_WORDS / 256, BATCH = PER < 16 ? PER : 16;
 #pragma unroll 1
     for (int b0 = 0; b0 < PER; b0 += BATCH) {
         u64 v[BATCH];
@@ -236,11 +244,11 @@ __global__ void __launch_bounds__(256) k_combine_t(CombineArgs p) {
     u64 *db = p.dst + (int64_t)blockIdx.z * 7 * p.dst_stride;
 #pragma unroll 1
     for (int half = 0; half < 2; ++half) {
-        u64 T[4][4];  // [quadrant][64-row group]: transposed word of row 64w + 32 half + lane
+        u64 T[4][NG];  // [quadrant][64-row group]: transposed word of row 64w + 32 half + lane
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd)
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
+            for (int g = 0; g < NG; ++g) {
                 const u64 x0 = tile[qd][64 * g + lane][warp], x1 = tile[qd][64 * g + 32 + lane][warp];
                 const uint32_t p0 = half ? (uint32_t)x0 : (uint32_t)(x0 >> 32);
                 const uint32_t p1 = half ? (uint32_t)x1 : (uint32_t)(x1 >> 32);
@@ -250,21 +258,21 @@ __global__ void __launch_bounds__(256) k_combine_t(CombineArgs p) {
         const int64_t orow = w * 64 + half * 32 + lane;  // output row (< 64 W, always in range)
 #pragma unroll
         for (int q = 0; q < 7; ++q) {
-            u64 o[4];
+            u64 o[NG];
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
+            for (int g = 0; g < NG; ++g) {
                 o[g] = 0;
 #pragma unroll
                 for (int qd = 0; qd < 4; ++qd)
                     if (p.mask[q] & (1u << qd)) o[g] ^= T[qd][g];
             }
             u64 *drow = db + q * p.dst_stride + orow * p.dst_pitch + r0 / 64;
-            if (vec) {
-                reinterpret_cast<ulonglong2 *>(drow)[0] = make_ulonglong2(o[0], o[1]);
-                reinterpret_cast<ulonglong2 *>(drow)[1] = make_ulonglong2(o[2], o[3]);
+            if (NG == 4 && vec) {
+                reinterpret_cast<ulonglong2 *>(drow)[0] = make_ulonglong2(o[0], o[NG > 1 ? 1 : 0]);
+                reinterpret_cast<ulonglong2 *>(drow)[1] = make_ulonglong2(o[NG > 2 ? 2 : 0], o[NG > 3 ? 3 : 0]);
             } else {
 #pragma unroll
-                for (int g = 0; g < 4; ++g)
+                for (int g = 0; g < NG; ++g)
                     if (g < ngroups) drow[g] = o[g];
             }
         }
@@ -384,11 +392,21 @@ int launch_combine_t(const CombineArgs &a, cudaStream_t s) {
     if (!a.R || !a.W || !a.nprob) return GF2_OK;
     if (a.R % 64) return set_error(GF2_ERR_PARAMETER, "combine_t: rows not a multiple of 64");
     static bool attr[64] = {};
-    if (first_on_device(attr))
-        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_combine_t, cudaFuncAttributeMaxDynamicSharedMemorySize, CT_SMEM),
-                           "combine_t smem attr"));
-    dim3 grd((unsigned)((a.W + CT_WORDS - 1) / CT_WORDS), (unsigned)((a.R + CT_ROWS - 1) / CT_ROWS), (unsigned)a.nprob);
-    GF2_LAUNCH(launch_k(k_combine_t, grd, 256, CT_SMEM, s, 1, a));
+    if (first_on_device(attr)) {
+        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_combine_t<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                ct_smem<256>()), "combine_t smem attr"));
+        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_combine_t<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                ct_smem<64>()), "combine_t smem attr"));
+    }
+    const int64_t gx = (a.W + CT_WORDS - 1) / CT_WORDS;
+    const int64_t big = gx * ((a.R + 255) / 256) * a.nprob;  // 256-row tiles
+    if (big >= 2 * num_sms()) {
+        dim3 grd((unsigned)gx, (unsigned)((a.R + 255) / 256), (unsigned)a.nprob);
+        GF2_LAUNCH(launch_k(k_combine_t<256>, grd, 256, ct_smem<256>(), s, 1, a));
+    } else {
+        dim3 grd((unsigned)gx, (unsigned)((a.R + 63) / 64), (unsigned)a.nprob);
+        GF2_LAUNCH(launch_k(k_combine_t<64>, grd, 256, ct_smem<64>(), s, 1, a));
+    }
     note_launch();
     return check_cuda(cudaGetLastError(), "k_combine_t launch");
 }
