@@ -251,7 +251,7 @@ def run_reference(args):
                 "d2h_bytes_per_step": 0},
         "note": "ms_per_step extrapolated to the full m rows",
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -373,8 +373,32 @@ def e2e_sharded(args, g, dev, stream, flush, a, r0, r1, w, params, world,
     return piped, serial
 
 
+_STDOUT_FD = None
+
+
+def _quiet_stdout():
+    """Point fd 1 at stderr for the run (NCCL / torch print banners such as
+    "NCCL version ..." to stdout) and keep the real stdout for the one JSON
+    line the driver parses."""
+    global _STDOUT_FD
+    if _STDOUT_FD is None:
+        sys.stdout.flush()
+        _STDOUT_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    text = json.dumps(line) + "\n"
+    if _STDOUT_FD is None:
+        print(text, end="", flush=True)
+    else:
+        sys.stdout.flush()
+        os.write(_STDOUT_FD, text.encode())
+
+
 def main():
     args = parse()
+    _quiet_stdout()
     if args.impl == "reference":
         run_reference(args)
         return
@@ -657,7 +681,7 @@ def main():
         "e2e_serial": e2e_serial,
         "vs_paper_2008_cpu": value / PAPER_2008_CPU,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     if dist_on:
         dist.destroy_process_group()
 
