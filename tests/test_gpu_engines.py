@@ -268,6 +268,44 @@ def test_unfused_post_additions(engine, digests):
     assert lines[-1] == "True"
 
 
+@pytest.mark.parametrize("env", [{"GF2_PDL": "0"}, {"GF2_F4_ORDER": "0"}, {"GF2_F4_ORDER": "3"}])
+def test_launch_and_raster_options(env, digests):
+    """The same results with programmatic dependent launch off (every kernel
+    then starts after its predecessor completes) and with the FP4 GEMM's
+    other tile rasters (column tiles fastest; blocks of 3 row tiles, a
+    ragged last block): cfg2 at cutoff 1024, cfg3 and a ragged addmul.
+    Options are read once per process, hence a subprocess."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import numpy as np\n"
+        "import paper_0811_1714_b200 as g\n"
+        "from oracle import gf2_oracle as O\n"
+        "from oracle import gf2_port as P\n"
+        "a, b = g.random(4096, 4096, 21), g.random(4096, 4096, 22)\n"
+        "print(O.digest(g.mul_strassen(a, b, g.MulParams(cutoff=1024, k=8)).to_numpy()))\n"
+        "a, b = g.random(16384, 16384, 31), g.random(16384, 16384, 32)\n"
+        "print(O.digest(g.mul_strassen(a, b).to_numpy()))\n"
+        "m, l, n = 5000, 4700, 5300\n"
+        "c = g.random(m, n, 3)\n"
+        "c0 = c.to_numpy().copy()\n"
+        "g.addmul(c, g.random(m, l, 1), g.random(l, n, 2), g.MulParams(cutoff=2048))\n"
+        "P.set_threads(P.max_threads())\n"
+        "want = P.mul_strassen(P.random(m, l, 1), P.random(l, n, 2), cutoff=2048).words\n"
+        "print(bool((c.to_numpy() == (c0 ^ want)).all()))\n"
+    ) % (root,)
+    out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), cwd=root,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = out.stdout.strip().splitlines()
+    assert lines[-3] == digests["cfg2"]
+    assert lines[-2] == digests["cfg3"]
+    assert lines[-1] == "True"
+
+
 @pytest.mark.parametrize("engine", ["m4rm", "tc-f4"])
 def test_deep_recursion_many_leaves(engine):
     """Fuzzer regression: cutoff 64 on 4546x12000x12000 recurses to depth 6

@@ -8,6 +8,8 @@ O=gpurun_out/fin
 mkdir -p $O
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/ref.json 2> $O/ref.err
+timeout 600 python bench.py --sharded --no-cpu-baseline > $O/sharded.json 2> $O/sharded.err
+timeout 600 python tools/shard_estimate.py > $O/shard_estimate.txt 2>&1
 timeout 1500 python tools/bench_configs.py > $O/configs.jsonl 2> $O/configs.err
 timeout 300 python tools/engine_cross.py > $O/cross_default.txt 2>&1
 GF2_TC_MIN_WORK=1e30 timeout 300 python tools/engine_cross.py > $O/cross_m4rm.txt 2>&1
