@@ -141,12 +141,22 @@ __global__ void __launch_bounds__(256) k_expand4_rows7(ExpandArgs a) {
 // 2 words: per 64-row K block, four warp-wide 32 x 32 transposes turn the
 // 64 x 64 bit block into 64 column K-vectors (lane: columns lane and lane + 32), and each lane writes
 // its two columns' 128 contiguous bytes (256 K entries).
-constexpr int F4T_ROWS = 256, F4T_WORDS = 16;
+// WORDS = 16 source words (1024 columns) per block, or 8 when 16-word tiles
+// would not give every SM a block: cfg2's 4096-column B 7.0 -> 5.3 us; the
+// wider tile stays better once the grid is larger (cfg4 17.2 vs 21.0 us).
+constexpr int F4T_ROWS = 256;
 constexpr int F4T_STG_PITCH = 144;  // 128 B output row + 16 B pad (conflict-free)
-constexpr int F4T_TILE_BYTES = F4T_ROWS * (F4T_WORDS + 1) * 8;
-constexpr int F4T_SMEM = F4T_TILE_BYTES + 8 * 32 * F4T_STG_PITCH;
-template <int LEVELS>
+template <int F4T_WORDS>
+constexpr int f4t_tile_bytes() {
+    return F4T_ROWS * (F4T_WORDS + 1) * 8;
+}
+template <int F4T_WORDS>
+constexpr int f4t_smem() {
+    return f4t_tile_bytes<F4T_WORDS>() + 8 * 32 * F4T_STG_PITCH;
+}
+template <int LEVELS, int F4T_WORDS>
 __global__ void __launch_bounds__(256) k_expand4_cols(ExpandArgs a) {
+    constexpr int F4T_TILE_BYTES = f4t_tile_bytes<F4T_WORDS>();
     pdl_begin();
     extern __shared__ __align__(16) unsigned char f4t_smem[];
     u64(*tile)[F4T_WORDS + 1] = reinterpret_cast<u64(*)[F4T_WORDS + 1]>(f4t_smem);
@@ -618,23 +628,35 @@ static int launch_expand4(const ExpandArgs &a, int64_t nprob, bool cols, cudaStr
             GF2_LAUNCH(launch_k(k_expand4_rows<2>, grd, 256, 0, s, 1, a));
     } else {
         // a.dp = bytes per K-major row = (K rows rounded to 64) / 2
-        dim3 grd((unsigned)((width + F4T_WORDS - 1) / F4T_WORDS), (unsigned)((a.dp * 2 + F4T_ROWS - 1) / F4T_ROWS),
-                 (unsigned)nprob);
+        const unsigned gy = (unsigned)((a.dp * 2 + F4T_ROWS - 1) / F4T_ROWS);
         static bool attr[64] = {};
         if (first_on_device(attr)) {
-            GF2_TRY(check_cuda(cudaFuncSetAttribute(k_expand4_cols<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    F4T_SMEM), "expand4 smem attr"));
-            GF2_TRY(check_cuda(cudaFuncSetAttribute(k_expand4_cols<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    F4T_SMEM), "expand4 smem attr"));
-            GF2_TRY(check_cuda(cudaFuncSetAttribute(k_expand4_cols<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    F4T_SMEM), "expand4 smem attr"));
+#define GF2_F4T_ATTR(L, W)                                                                                     \
+    GF2_TRY(check_cuda(cudaFuncSetAttribute(k_expand4_cols<L, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                            f4t_smem<W>()),                                                     \
+                       "expand4 smem attr"))
+            GF2_F4T_ATTR(0, 16); GF2_F4T_ATTR(1, 16); GF2_F4T_ATTR(2, 16);
+            GF2_F4T_ATTR(0, 8); GF2_F4T_ATTR(1, 8); GF2_F4T_ATTR(2, 8);
+#undef GF2_F4T_ATTR
         }
-        if (a.levels == 0)
-            GF2_LAUNCH(launch_k(k_expand4_cols<0>, grd, 256, F4T_SMEM, s, 1, a));
-        else if (a.levels == 1)
-            GF2_LAUNCH(launch_k(k_expand4_cols<1>, grd, 256, F4T_SMEM, s, 1, a));
-        else
-            GF2_LAUNCH(launch_k(k_expand4_cols<2>, grd, 256, F4T_SMEM, s, 1, a));
+        const int64_t wide = (width + 15) / 16 * (int64_t)gy * nprob;  // blocks with 16-word tiles
+        if (wide >= num_sms()) {
+            dim3 grd((unsigned)((width + 15) / 16), gy, (unsigned)nprob);
+            if (a.levels == 0)
+                GF2_LAUNCH(launch_k(k_expand4_cols<0, 16>, grd, 256, f4t_smem<16>(), s, 1, a));
+            else if (a.levels == 1)
+                GF2_LAUNCH(launch_k(k_expand4_cols<1, 16>, grd, 256, f4t_smem<16>(), s, 1, a));
+            else
+                GF2_LAUNCH(launch_k(k_expand4_cols<2, 16>, grd, 256, f4t_smem<16>(), s, 1, a));
+        } else {
+            dim3 grd((unsigned)((width + 7) / 8), gy, (unsigned)nprob);
+            if (a.levels == 0)
+                GF2_LAUNCH(launch_k(k_expand4_cols<0, 8>, grd, 256, f4t_smem<8>(), s, 1, a));
+            else if (a.levels == 1)
+                GF2_LAUNCH(launch_k(k_expand4_cols<1, 8>, grd, 256, f4t_smem<8>(), s, 1, a));
+            else
+                GF2_LAUNCH(launch_k(k_expand4_cols<2, 8>, grd, 256, f4t_smem<8>(), s, 1, a));
+        }
     }
     note_launch();
     return check_cuda(cudaGetLastError(), "k_expand4 launch");
