@@ -275,59 +275,21 @@ __device__ __forceinline__ void umma_f4(uint32_t taddr, uint64_t ad, uint64_t bd
         "l"(ad), "l"(bd), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb));
 }
 
-// 32-bit group g of a row (columns 32g..32g+31, MSB-first) is u32 index g^1
-// of the row's little-endian 64-bit words.
+// Plain store (no accumulation) of a row's tile groups: group g (columns
+// 32g..32g+31, MSB-first) is u32 index g^1 of the row's little-endian 64-bit
+// words; a partial last group keeps the bits beyond n. XOR-accumulation
+// (accumulate, K chunks, fused post-additions) goes through xor_rows_f4.
 __device__ __forceinline__ void store_row_f4(const UArgs &p, const uint32_t *packed, int64_t row, int64_t g0,
                                              int nch, int64_t gprob) {
     if (row >= p.m) return;
-    uint32_t v[F4_BN / 32];
-    uint32_t keep[F4_BN / 32];
-#pragma unroll
-    for (int c = 0; c < F4_BN / 32; ++c) {
-        const int64_t rem = p.n - (g0 + c) * 32;
-        v[c] = (c < nch && rem > 0) ? packed[c] : 0u;
-        keep[c] = (c < nch && rem > 0 && rem < 32) ? (~0u >> rem) : 0u;
-        if (keep[c]) v[c] &= ~keep[c];
-    }
-    // XOR-accumulate into a row: adjacent groups (2w, 2w+1) share the
-    // 64-bit word w (group 2w in its high half), so they go out as one
-    // red.xor.b64 -- 4 atomics per row instead of 7. The start group's
-    // parity is warp-uniform; both cases are unrolled so v[] stays in
-    // registers. A zero half contributed to a neighbour's word is a no-op.
-    auto red_row = [&](u64 *crow) {
-        if ((g0 & 1) == 0) {
-#pragma unroll
-            for (int c = 0; c < F4_BN / 32; c += 2) {
-                const u64 x = ((u64)v[c] << 32) | (c + 1 < F4_BN / 32 ? v[c + 1] : 0u);
-                if (x) atomicXor(reinterpret_cast<unsigned long long *>(crow + (g0 + c) / 2), (unsigned long long)x);
-            }
-        } else {
-            if (v[0]) atomicXor(reinterpret_cast<unsigned *>(crow) + (g0 ^ 1), v[0]);
-#pragma unroll
-            for (int c = 1; c < F4_BN / 32; c += 2) {
-                const u64 x = ((u64)v[c] << 32) | v[c + 1];
-                if (x) atomicXor(reinterpret_cast<unsigned long long *>(crow + (g0 + c) / 2), (unsigned long long)x);
-            }
-        }
-    };
-    if (p.post) {
-        const unsigned dm = p.post_mask[gprob % 7];
-        u64 *cbase = p.C + (gprob / 7) * p.sc + row * p.pc;
-#pragma unroll
-        for (int Q = 0; Q < 4; ++Q)
-            if (dm & (1u << Q)) red_row(cbase + p.qoffC[Q]);
-        return;
-    }
-    if (p.mode >= 1) {  // XOR-accumulate (1) or K-chunk partials (2): fire-and-forget
-        red_row(p.C + gprob * p.sc + row * p.pc);
-        return;
-    }
     unsigned *crow = reinterpret_cast<unsigned *>(p.C + gprob * p.sc + row * p.pc);
 #pragma unroll
     for (int c = 0; c < F4_BN / 32; ++c) {
-        if (c >= nch || (g0 + c) * 32 >= p.n) break;
+        const int64_t rem = p.n - (g0 + c) * 32;
+        if (c >= nch || rem <= 0) break;
+        const uint32_t keep = rem < 32 ? (~0u >> rem) : 0u;
         unsigned *w = crow + ((g0 + c) ^ 1);
-        *w = keep[c] ? ((*w & keep[c]) | v[c]) : v[c];
+        *w = keep ? ((*w & keep) | (packed[c] & ~keep)) : packed[c];
     }
 }
 
@@ -555,11 +517,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
             mbar_wait(bar_tfull + 8 * acc, acc_phase);
             tc_fence_after();
             // 32-column groups, software-pipelined: group c+1's TMEM load is
-            // in flight while group c's parities are packed. Packing has no
-            // serial chain: each column's parity is shifted into place on its
-            // own and OR-ed into one of 4 partial words (4-deep LOP3 chains
-            // instead of a 64-deep shift-or chain per group), so small-K tiles
-            // are no longer epilogue-bound.
+            // in flight while group c's parities are packed (parity_pack32).
             if (p.dbg == 2) {
                 tc_fence_before();
                 mbar_arrive_leader(bar_tempty + 8 * acc);
