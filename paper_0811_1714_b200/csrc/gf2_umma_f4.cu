@@ -570,8 +570,16 @@ static int launch_expand4(const ExpandArgs &a, int64_t nprob, bool cols, cudaStr
     if (!cols && a.levels == 1 && a.q0 % 7 == 0 && nprob % 7 == 0) {
         // 2 rows per warp: 48 registers, more resident blocks and a finer grid
         // than 4 (43 vs 45 us at cfg3; forcing occupancy via launch bounds spills)
-        dim3 grd((unsigned)((width + 31) / 32), (unsigned)((a.rows + 8 * 2 - 1) / (8 * 2)), (unsigned)(nprob / 7));
-        GF2_LAUNCH(launch_k(k_expand4_rows7<2>, grd, 256, 0, s, 1, a));
+        // one row per warp when two would give fewer than 4 blocks per SM
+        // (cfg2 at cutoff 1024: 448 blocks; 16.8 -> 15.0 us for both sides)
+        const int64_t blocks2 = (width + 31) / 32 * ((a.rows + 15) / 16) * (nprob / 7);
+        if (blocks2 < 4 * num_sms()) {
+            dim3 grd((unsigned)((width + 31) / 32), (unsigned)((a.rows + 8 - 1) / 8), (unsigned)(nprob / 7));
+            GF2_LAUNCH(launch_k(k_expand4_rows7<1>, grd, 256, 0, s, 1, a));
+        } else {
+            dim3 grd((unsigned)((width + 31) / 32), (unsigned)((a.rows + 8 * 2 - 1) / (8 * 2)), (unsigned)(nprob / 7));
+            GF2_LAUNCH(launch_k(k_expand4_rows7<2>, grd, 256, 0, s, 1, a));
+        }
         note_launch();
         return check_cuda(cudaGetLastError(), "k_expand4_rows7 launch");
     }
