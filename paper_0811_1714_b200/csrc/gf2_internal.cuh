@@ -229,10 +229,13 @@ inline double tensor_min_work() {
     return g_engine == 3 ? 1.0e10 : 17179869184.0;
 }
 // smallest leaf side for tensor-core Strassen leaves (GF2_TC_MIN_LEAF
-// overrides it; tests use 256 to drive 117649 tensor leaves through chunking)
+// overrides it; tests use 256 to drive 117649 tensor leaves through chunking).
+// 640: 3000^3 at cutoff 512 (736-side leaves) 104.7 -> 88.3 us on tensor
+// leaves, while 4096^3 at cutoff 512 (512-side leaves) stays faster on M4RM
+// (112.9 vs 121.1 us; tools/leaf_cross.py)
 inline int64_t tensor_min_leaf() {
     static const int64_t env = getenv("GF2_TC_MIN_LEAF") ? atoll(getenv("GF2_TC_MIN_LEAF")) : 0;
-    return env > 0 ? env : 1024;
+    return env > 0 ? env : 640;
 }
 inline int launch_product(const M4rmBatch &b, cudaStream_t s) {
     const double work = (double)b.m * (double)b.l * (double)b.n * (double)b.nprob;

@@ -234,9 +234,8 @@ int strassen_core(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0, in
                   cudaStream_t s) {
     if (g_engine != 0) {
         // tensor-core leaves when the batch is big enough to amortize the
-        // expansion and each leaf is at least 1024 on every side (smaller
-        // leaves run faster on M4RM: 3000^3 at cutoff 512, 138 vs 154 us,
-        // tools/engine_cross.py)
+        // expansion and each leaf is at least tensor_min_leaf() (640) on every
+        // side; smaller leaves run faster on M4RM
         const int64_t lm = A0.nrows >> depth, ll = A0.ncols >> depth, ln = B0.ncols >> depth;
         double leaf = (double)lm * (double)ll * (double)ln;
         for (int i = 0; i < depth; ++i) leaf *= 7.0;
