@@ -239,7 +239,12 @@ def _check_cuda_dev(*mats):
 
 
 def _storage(m):
-    return m.storage if isinstance(m, BitMatrix) else m.parent.storage
+    if isinstance(m, BitMatrix):
+        return m.storage
+    if isinstance(m, MatrixWindow):
+        return m.parent.storage
+    raise TypeError(f"expected a device BitMatrix or MatrixWindow, got {type(m).__name__} "
+                    "(upload host matrices with from_host)")
 
 
 # ------------------------------------------------------------ constructors
