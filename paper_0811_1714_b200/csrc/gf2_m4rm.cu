@@ -236,10 +236,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 u64 c0 = 0, c1 = 0, y0, y1;
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {  // slot bits 7..4 <-> source rows 0..3
-                    lds128(srow + i * kRowBytes, y0, y1);
-                    const u64 sel = (r0 & (8 >> i)) ? ~0ULL : 0ULL;
-                    c0 ^= y0 & bm0 & sel;
-                    c1 ^= y1 & bm1 & sel;
+                    // only the rows in this slot group's high bits are read:
+                    // the lanes of other groups skip the load, which saves
+                    // shared-memory wavefronts (the kernel's binding resource)
+                    if (r0 & (8 >> i)) {
+                        lds128(srow + i * kRowBytes, y0, y1);
+                        c0 ^= y0 & bm0;
+                        c1 ^= y1 & bm1;
+                    }
                 }
                 u64 x0[4], x1[4];  // slot bits 3..0 <-> source rows 4..7
 #pragma unroll
