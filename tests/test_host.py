@@ -85,3 +85,28 @@ def test_gf2m_load_errors_match_reference(golden, tmp_path):
         with pytest.raises(FormatError) as exc:
             load(fp)
         assert str(exc.value) == want[name], name
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference (CPU only): exactly one JSON line on stdout
+    with the contract's keys on rank 0; other ranks print nothing and exit 0."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--size", "1024",
+           "--steps", "1", "--warmup", "0"]
+    out = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = out.stdout.splitlines()
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
+    for k in ("metric", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "cpu_baseline", "e2e", "config"):
+        assert k in d, k
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    other = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=300,
+                           env=dict(os.environ, RANK="1", WORLD_SIZE="2"))
+    assert other.returncode == 0 and other.stdout == ""
