@@ -65,6 +65,10 @@ const char *gf2_last_error(void);
  * Call it outside ncclGroupStart/End, from one host thread or process per
  * GPU: the per-panel "landed" events are recorded right after each
  * ncclBroadcast is issued, which a group would defer.
+ * `b` may be any view and the ranks' pitches may differ: a B whose pitch is
+ * not its width in words (a window, or a padded pitch) travels through a
+ * contiguous staging buffer and is unpacked with an edge-preserving copy,
+ * so no word outside B's window is written on any rank.
  * The Python package offers the same over torch.distributed
  * (paper_0811_1714_b200.sharded.mul_sharded). */
 int gf2_mul_sharded(const gf2_view *c_shard, const gf2_view *a_shard, const gf2_view *b, void *nccl_comm,
@@ -125,6 +129,30 @@ int gf2_copy(const gf2_view *out, const gf2_view *a, void *stream);
  * alias A or B. */
 int gf2_m4rm(const gf2_view *c, const gf2_view *a, const gf2_view *b, int k,
              int accumulate, void *stream);
+
+/* m4rm.py:124-155 `mul_m4rm*` as the drop-in runs them (m4rm.py:77-121
+ * `_mul_into` semantics, C = A.B or C ^= A.B): one base-case product, no
+ * recursion, on the M4RM kernel -- or, past the measured crossover (>= 1e10
+ * bit-ops and every side >= 640), on the selected tensor engine, where the
+ * same product is faster. Engine 0 (M4RM) forces the M4RM kernel. Same
+ * arguments, semantics and errors as gf2_m4rm. */
+int gf2_mul_base(const gf2_view *c, const gf2_view *a, const gf2_view *b, int k,
+                 int accumulate, void *stream);
+
+/* graycode.py:108-156 `make_table`: table rows [0, 2^k) = every XOR
+ * combination of the k rows of `src` (pass the view of rows
+ * [start_row, start_row + k) of B); slot x holds the XOR of the rows i with
+ * bit k-1-i of x set (big-endian, slot 0 = zero). Bits of `src` beyond its
+ * right edge are masked; the table's rows stay clean. `table` must hold at
+ * least 2^k rows of src->ncols columns and must not alias src. */
+int gf2_make_table(const gf2_view *table, const gf2_view *src, int k, void *stream);
+
+/* strassen.py:219-249 `peel_fixup`: complete C = A.B given that
+ * C[:m2, :n2] already holds A[:m2, :l2] . B[:l2, :n2]: the inner remainder
+ * is accumulated into that block, then the bottom rows and the right
+ * columns are written, each as one base-case product (never the recursion). */
+int gf2_peel_fixup(const gf2_view *c, const gf2_view *a, const gf2_view *b,
+                   int64_t m2, int64_t l2, int64_t n2, void *stream);
 
 /* One product launch (no recursion) with the current engine (gf2_set_engine):
  * the dense-contraction entry of north_star (c) when a tensor engine is set.
@@ -187,7 +215,8 @@ int gf2_timer_enable(int on);
  * process-wide: 0 = M4RM shared-memory Gray tables, 1 = tcgen05 kind::i8
  * (u8 0/1), 2 = tcgen05 kind::f8f6f4 (e4m3 0/1), 3 = tcgen05 kind::mxf4
  * (e2m1 nibbles, unit block scales; default: measured fastest).
- * gf2_m4rm always runs the M4RM kernel. Results are identical. */
+ * gf2_m4rm always runs the M4RM kernel; gf2_mul_base (the mul_m4rm* path)
+ * uses the tensor engine past the crossover. Results are identical. */
 int gf2_set_engine(int engine);
 int gf2_get_engine(void);
 int gf2_timer_read(double *kernel_ms, double *bitops, int64_t *launches);

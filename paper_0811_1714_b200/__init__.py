@@ -13,16 +13,19 @@ from ._lib import (DeviceError, NativeUnavailable, get_engine, launch_count,
 from .core import (BitMatrix, HostMatrix, MatrixWindow, add, add_into,
                    bernoulli, copy_into, copy_out, create, equal,
                    first_difference, from_dense, from_host, from_numpy,
-                   identity, random, tail_mask, to_dense, to_numpy,
-                   trailing_bits_clean, window, words_per_row, zero_into)
+                   identity, random, random_into, tail_mask, to_dense,
+                   to_numpy, trailing_bits_clean, window, words_per_row,
+                   zero_into)
 from .errors import (AlignmentError, DimensionError, FormatError, GF2MatError,
                      ParameterError)
 from .m4rm import (StripeSpec, mul_m4rm, mul_m4rm_blocked, mul_m4rm_into,
                    mul_m4rm_multitable)
 from .gf2m import load, save
+from .graycode import CombinationTable, GrayCode, build_gray, make_table
 from .strassen import (GPU_CUTOFF, MulParams, PeelSplit, StrassenPlan,
-                       addmul, addmul_direct, default_params, mul_direct,
-                       mul_strassen, peel_split)
+                       addmul, addmul_direct, choose_k, default_params,
+                       mul_direct, mul_strassen, peel_fixup, peel_split,
+                       schedule_winograd)
 from .structure import augment, mul_cubic, stack, transpose
 
 __version__ = "0.1.0"
@@ -41,4 +44,6 @@ __all__ = [
     "to_dense",
     "to_numpy", "trailing_bits_clean", "window", "words_per_row", "zero_into",
     "augment", "load", "mul_cubic", "save", "stack", "transpose",
+    "CombinationTable", "GrayCode", "build_gray", "make_table", "choose_k",
+    "peel_fixup", "schedule_winograd", "random_into",
 ]

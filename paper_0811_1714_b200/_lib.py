@@ -57,6 +57,10 @@ SIGNATURES = {
     "gf2_copy": (ctypes.c_int, [_V, _V, _P]),
     "gf2_m4rm": (ctypes.c_int, [_V, _V, _V, ctypes.c_int, ctypes.c_int, _P]),
     "gf2_mul": (ctypes.c_int, [_V, _V, _V, ctypes.c_int, _P]),
+    "gf2_mul_base": (ctypes.c_int, [_V, _V, _V, ctypes.c_int, ctypes.c_int, _P]),
+    "gf2_make_table": (ctypes.c_int, [_V, _V, ctypes.c_int, _P]),
+    "gf2_peel_fixup": (ctypes.c_int, [_V, _V, _V, ctypes.c_int64, ctypes.c_int64,
+                                      ctypes.c_int64, _P]),
     "gf2_transpose": (ctypes.c_int, [_V, _V, _P]),
     "gf2_cubic": (ctypes.c_int, [_V, _V, _V, ctypes.c_int, _P]),
     "gf2_copy_cols": (ctypes.c_int, [_V, ctypes.c_int64, _V, _P]),

@@ -216,6 +216,10 @@ def _to_host(m):
     imported the reference package, else a HostMatrix with the same
     attribute surface. This package never imports gf2mat itself."""
     words = m.to_numpy()
+    if words.size:
+        # a window's last word may carry its parent's bits beyond the right
+        # edge; an owned copy keeps the clean-tail invariant (core.py:335-341)
+        words[:, -1] &= np.uint64(tail_mask(m.ncols))
     ref = sys.modules.get("gf2mat")
     if ref is not None and hasattr(ref, "create"):
         out = ref.create(m.nrows, m.ncols)
@@ -229,13 +233,33 @@ def _stream():
     return _lib.current_stream()
 
 
+_cur_dev = None
+
+
+def _current_device() -> int:
+    global _cur_dev
+    if _cur_dev is None:
+        c = _torch()._C
+        _cur_dev = getattr(c, "_cuda_getDevice", None) or \
+            _torch().cuda.current_device
+    return _cur_dev()
+
+
 def _check_cuda_dev(*mats):
-    # device indices, compared without building torch.device objects
+    """Every operand on one device, and that device the current one: each
+    operation runs on the current device's current stream, so device-1
+    pointers launched from device 0 would fault (compared as indices,
+    without building torch.device objects)."""
     d0 = _storage(mats[0]).get_device()
     for m in mats[1:]:
         if _storage(m).get_device() != d0:
             devs = {str(x.device) for x in mats}
             raise DimensionError(f"operands live on different devices: {devs}")
+    cur = _current_device()
+    if d0 != cur:
+        raise DimensionError(
+            f"operands live on cuda:{d0} but the current device is cuda:{cur}; "
+            f"run under torch.cuda.device({d0})")
 
 
 def _storage(m):
@@ -260,9 +284,21 @@ def random(nrows: int, ncols: int, seed: int, device=None,
     matrix with the same seed -- how row shards are generated in place."""
     m = BitMatrix(nrows, ncols, device)
     if m.nrows and m.width:
+        _check_cuda_dev(m)
         _lib.check(_lib.lib_cuda().gf2_random(
             m._view(), seed & _FULL, row_base, _stream()))
     return m
+
+
+def random_into(out: BitMatrix, seed: int, row_base: int = 0) -> None:
+    """Refill an owned matrix with `random(out.nrows, out.ncols, seed,
+    row_base=row_base)` in place (no allocation)."""
+    if not isinstance(out, BitMatrix):
+        raise TypeError("random_into fills an owned BitMatrix")
+    if out.nrows and out.width:
+        _check_cuda_dev(out)
+        _lib.check(_lib.lib_cuda().gf2_random(
+            out._view(), seed & _FULL, row_base, _stream()))
 
 
 def bernoulli(nrows: int, ncols: int, seed: int, p: float | None = None,
@@ -277,6 +313,7 @@ def bernoulli(nrows: int, ncols: int, seed: int, p: float | None = None,
         threshold = _FULL if p >= 1 else int(Fraction(str(p)) * (1 << 64))
     m = BitMatrix(nrows, ncols, device)
     if m.nrows and m.width:
+        _check_cuda_dev(m)
         _lib.check(_lib.lib_cuda().gf2_bernoulli(
             m._view(), seed & _FULL, threshold & _FULL, row_base, _stream()))
     return m
@@ -318,6 +355,7 @@ def from_numpy(words: np.ndarray, ncols: int, device=None,
         if words.strides[1] != 8 or words.strides[0] % 8:
             words = np.ascontiguousarray(words)
             nonblocking = False
+        _check_cuda_dev(m)
         _lib.check(_lib.lib_cuda().gf2_upload(
             m._view(), words.ctypes.data, words.strides[0] // 8, _stream()))
         if not nonblocking:
@@ -346,6 +384,7 @@ def _download(a: Mat, out: np.ndarray | None,
             or out.strides[1] != 8:
         raise DimensionError(f"download buffer {out.shape} != ({a.nrows}, {w})")
     if a.nrows and w:
+        _check_cuda_dev(a)
         _lib.check(_lib.lib_cuda().gf2_download(
             a._view(), out.ctypes.data, out.strides[0] // 8, _stream()))
         if not nonblocking:
@@ -416,6 +455,7 @@ def copy_out(w: Mat) -> BitMatrix:
 
 
 def zero_into(out: Mat) -> None:
+    _check_cuda_dev(out)
     _lib.check(_lib.lib_cuda().gf2_zero(out._view(), _stream()))
 
 

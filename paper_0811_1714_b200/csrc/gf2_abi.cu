@@ -235,6 +235,40 @@ int gf2_m4rm(const gf2_view *c, const gf2_view *a, const gf2_view *b, int k, int
     return m4rm_mul(*c, *a, *b, accumulate ? 1 : 0, (cudaStream_t)stream);
 }
 
+int gf2_mul_base(const gf2_view *c, const gf2_view *a, const gf2_view *b, int k, int accumulate, void *stream) {
+    if (k < 1 || k > 16) return set_error(GF2_ERR_PARAMETER, "k=" + std::to_string(k) + " outside 1..16");
+    GF2_TRY(check_mul(c, a, b));
+    return base_mul(*c, *a, *b, accumulate ? 1 : 0, (cudaStream_t)stream);
+}
+
+int gf2_make_table(const gf2_view *table, const gf2_view *src, int k, void *stream) {
+    GF2_TRY(check_view(table, "table"));
+    GF2_TRY(check_view(src, "src"));
+    if (k < 1 || k > 16) return set_error(GF2_ERR_PARAMETER, "table fill width " + std::to_string(k) +
+                                                                 " outside 1..16");
+    if (src->nrows != k)
+        return set_error(GF2_ERR_DIMENSION, "source holds " + std::to_string(src->nrows) + " rows, k=" +
+                                                std::to_string(k));
+    if (table->ncols != src->ncols)  // graycode.py:128-130
+        return set_error(GF2_ERR_DIMENSION, "table width " + std::to_string(table->ncols) + " != source width " +
+                                                std::to_string(src->ncols));
+    if (table->nrows < ((int64_t)1 << k))
+        return set_error(GF2_ERR_DIMENSION, "table holds " + std::to_string(table->nrows) + " rows < 2^" +
+                                                std::to_string(k));
+    if (overlaps(*table, *src)) return set_error(GF2_ERR_PARAMETER, "table aliases its source rows");
+    return launch_make_table(*table, *src, k, (cudaStream_t)stream);
+}
+
+int gf2_peel_fixup(const gf2_view *c, const gf2_view *a, const gf2_view *b, int64_t m2, int64_t l2, int64_t n2,
+                   void *stream) {
+    GF2_TRY(check_mul(c, a, b));
+    if (m2 < 0 || l2 < 0 || n2 < 0 || m2 > a->nrows || l2 > a->ncols || n2 > b->ncols)  // strassen.py:234-236
+        return set_error(GF2_ERR_DIMENSION, "peel dims (" + std::to_string(m2) + "," + std::to_string(l2) + "," +
+                                                std::to_string(n2) + ") exceed (" + std::to_string(a->nrows) + "," +
+                                                std::to_string(a->ncols) + "," + std::to_string(b->ncols) + ")");
+    return peel_fixup(*c, *a, *b, m2, l2, n2, 0, (cudaStream_t)stream);
+}
+
 int gf2_mul(const gf2_view *c, const gf2_view *a, const gf2_view *b, int accumulate, void *stream) {
     GF2_TRY(check_mul(c, a, b));
     return engine_mul(*c, *a, *b, accumulate ? 1 : 0, (cudaStream_t)stream);

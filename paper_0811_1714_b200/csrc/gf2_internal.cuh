@@ -143,6 +143,7 @@ int launch_random(const gf2_view &v, u64 seed, int64_t row_base, cudaStream_t s)
 int launch_bernoulli(const gf2_view &v, u64 seed, u64 thresh, int64_t row_base, cudaStream_t s);
 int launch_ewise(const gf2_view &out, const gf2_view *a, const gf2_view *b, int op, cudaStream_t s);
 int launch_zero(const gf2_view &v, cudaStream_t s);
+int launch_make_table(const gf2_view &table, const gf2_view &src, int k, cudaStream_t s);  // graycode.py:108-156
 
 // Batched XOR-combine used by the breadth-first Strassen-Winograd:
 // for output o = p * nq + q (p < nprob, q < nq):
@@ -211,6 +212,11 @@ struct UmmaJob {
     cudaEvent_t b_ready;  // if set: B's source is produced on another stream
 };
 int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s);
+// strassen.py:219-249 (acc_rest: XOR the bottom rows / right columns in)
+int peel_fixup(const gf2_view &C, const gf2_view &A, const gf2_view &B, int64_t m2, int64_t l2, int64_t n2,
+               int acc_rest, cudaStream_t s);
+// one base-case product at the measured M4RM / tensor-engine crossover
+int base_mul(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accumulate, cudaStream_t s);
 int launch_umma_f4(const UmmaJob &jb, int64_t nprob, cudaStream_t s);  // gf2_umma_f4.cu
 int num_sms();
 // multiply engine for every product (gf2_set_engine): 0 M4RM, 1 tcgen05 i8, 2 tcgen05 f8, 3 tcgen05 mxf4

@@ -294,6 +294,33 @@ inline dim3 row_block(int64_t width) {
     return dim3(8, 32, 1);
 }
 
+
+// graycode.py:108-156 -- the 2^k-slot table of all XOR combinations of k
+// source rows, slot x = XOR of rows i with bit (k-1-i) of x set (big-endian:
+// bit k-1 is the first row), slot 0 = 0. Source words are masked with the
+// tail mask (a window source may carry live bits beyond its right edge).
+// A thread owns one word column of one group of 2^kl slots (kl = min(k, 8)):
+// it XORs the group's high-bit rows once, then walks the low kl bits in Gray
+// order -- one row XOR per slot, as the reference's table steps.
+__global__ void k_make_table(u64 *T, int64_t tp, const u64 *src, int64_t sp, int k, int kl,
+                             int64_t width, u64 tm) {
+    pdl_begin();
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= width) return;
+    const u64 m = j == width - 1 ? tm : ~0ULL;
+    const int64_t hi = blockIdx.y;             // the slot bits above the low kl
+    u64 acc = 0;
+    for (int b = kl; b < k; ++b)               // bit b of the slot <-> source row k-1-b
+        if ((hi >> (b - kl)) & 1) acc ^= src[(int64_t)(k - 1 - b) * sp + j] & m;
+    const int64_t base = hi << kl;
+    T[base * tp + j] = acc;
+    for (int64_t t = 1; t < ((int64_t)1 << kl); ++t) {
+        const int b = __ffsll(t) - 1;          // the bit that flips at Gray step t
+        acc ^= src[(int64_t)(k - 1 - b) * sp + j] & m;
+        T[(base | (t ^ (t >> 1))) * tp + j] = acc;
+    }
+}
+
 }  // namespace
 
 int launch_random(const gf2_view &v, u64 seed, int64_t row_base, cudaStream_t s) {
@@ -336,6 +363,18 @@ int launch_ewise(const gf2_view &out, const gf2_view *a, const gf2_view *b, int 
 
 // Zero a view: a 2-D memset when it covers whole words, else the masked
 // k_ewise (bits beyond a ragged right edge belong to the parent matrix).
+int launch_make_table(const gf2_view &table, const gf2_view &src, int k, cudaStream_t s) {
+    const int64_t width = words_per_row(src.ncols);
+    if (!width) return GF2_OK;
+    const int kl = k < 8 ? k : 8;
+    const dim3 blk((unsigned)(width < 128 ? ((width + 31) / 32) * 32 : 128));
+    const dim3 grd((unsigned)((width + blk.x - 1) / blk.x), 1u << (k - kl));
+    GF2_LAUNCH(launch_k(k_make_table, grd, blk, 0, s, 1, table.data, table.pitch, (const u64 *)src.data,
+                        src.pitch, k, kl, width, tail_mask(src.ncols)));
+    note_launch();
+    return check_cuda(cudaGetLastError(), "k_make_table launch");
+}
+
 int launch_zero(const gf2_view &v, cudaStream_t s) {
     if (!v.nrows || !v.ncols) return GF2_OK;
     if (v.ncols % kWordBits) return launch_ewise(v, nullptr, nullptr, 0, s);

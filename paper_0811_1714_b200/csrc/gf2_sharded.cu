@@ -103,14 +103,35 @@ int mul_sharded(const gf2_view &c, const gf2_view &a, const gf2_view &b, ncclCom
     }
     CommStream *cs = nullptr;
     GF2_TRY(comm_stream(&cs, pieces.size()));
+    // B goes over the wire as whole rows of `width` words. A B whose pitch is
+    // its width (an owned matrix without padding words, or whole rows of
+    // one) is broadcast in place. Any other B -- a window at a word offset,
+    // a ragged window, or a padded pitch -- is staged through a contiguous
+    // buffer: packed here, broadcast, and unpacked with the edge-preserving
+    // copy, so no word outside B's window is written and the byte counts do
+    // not depend on each rank's pitch.
+    const int64_t W = words_per_row(b.ncols);
+    const bool staged = b.pitch != W;
+    u64 *stage = nullptr;
+    if (staged) {
+        cudaError_t e = cudaMallocAsync((void **)&stage, (size_t)(b.nrows * W) * 8, s);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return set_error(GF2_ERR_OOM, std::string("sharded B staging: ") + cudaGetErrorString(e));
+        }
+        const gf2_view sv{stage, W, b.nrows, b.ncols};
+        GF2_TRY(launch_ewise(sv, &b, nullptr, 1, s));
+    }
+    u64 *wire = staged ? stage : b.data;
+    const int64_t wp = staged ? W : b.pitch;
     // the broadcast may overwrite B only after earlier work on `s` is done
     cudaEvent_t ready = cs->landed[0];
     GF2_TRY(check_cuda(cudaEventRecord(ready, s), "ready"));
     GF2_TRY(check_cuda(cudaStreamWaitEvent(cs->s, ready, 0), "ready wait"));
     for (size_t i = 0; i < pieces.size(); ++i) {
         const int64_t k0 = pieces[i].first, k1 = pieces[i].second;
-        // rows k0..k1 of B, whole pitched rows: one contiguous byte range
-        GF2_TRY(check_nccl(g_bcast(b.data + k0 * b.pitch, b.data + k0 * b.pitch, (size_t)((k1 - k0) * b.pitch) * 8,
+        // rows k0..k1 of B: one contiguous byte range
+        GF2_TRY(check_nccl(g_bcast(wire + k0 * wp, wire + k0 * wp, (size_t)((k1 - k0) * wp) * 8,
                                    ncclUint8, src >= 0 ? src : (int)i, comm, cs->s),
                            "ncclBroadcast"));
         GF2_TRY(check_cuda(cudaEventRecord(cs->landed[i], cs->s), "panel landed"));
@@ -118,11 +139,18 @@ int mul_sharded(const gf2_view &c, const gf2_view &a, const gf2_view &b, ncclCom
     size_t next = 0;
     for (size_t i = 0; i < panels.size(); ++i) {
         const int64_t k0 = panels[i].first, k1 = panels[i].second;
-        for (; next < pieces.size() && pieces[next].first < k1; ++next)
+        for (; next < pieces.size() && pieces[next].first < k1; ++next) {
             GF2_TRY(check_cuda(cudaStreamWaitEvent(s, cs->landed[next], 0), "panel wait"));
+            if (staged) {
+                const int64_t p0 = pieces[next].first, p1 = pieces[next].second;
+                const gf2_view sv{stage + p0 * W, W, p1 - p0, b.ncols};
+                GF2_TRY(launch_ewise(sub_view(b, p0, 0, p1 - p0, b.ncols), &sv, nullptr, 1, s));
+            }
+        }
         GF2_TRY(strassen_mul(c, sub_view(a, 0, k0, a.nrows, k1 - k0), sub_view(b, k0, 0, k1 - k0, b.ncols), cutoff,
                              1, s));
     }
+    if (staged) GF2_TRY(check_cuda(cudaFreeAsync(stage, s), "free staging"));
     return GF2_OK;
 }
 

@@ -395,16 +395,39 @@ int strassen_mul(const gf2_view &C, const gf2_view &A, const gf2_view &B, int64_
     const int64_t m2 = ps[0], l2 = ps[1], n2 = ps[2];
     GF2_TRY(strassen_core(sub_view(C, 0, 0, m2, n2), sub_view(A, 0, 0, m2, l2), sub_view(B, 0, 0, l2, n2),
                           (int)ps[3], accumulate, s));
-    // peel_fixup: inner remainder (accumulate), bottom rows, right columns
-    if (l2 < l)
+    return peel_fixup(C, A, B, m2, l2, n2, accumulate, s);
+}
+
+// strassen.py:219-249 `peel_fixup`: complete C given that C[:m2, :n2] holds
+// A[:m2, :l2] . B[:l2, :n2] -- the inner remainder accumulated into that
+// block, then the bottom rows, then the right columns, each one base-case
+// product (never the recursion). acc_rest = 1 XORs the bottom rows and right
+// columns into C instead of overwriting them (C += A.B).
+int peel_fixup(const gf2_view &C, const gf2_view &A, const gf2_view &B, int64_t m2, int64_t l2, int64_t n2,
+               int acc_rest, cudaStream_t s) {
+    const int64_t m = A.nrows, l = A.ncols, n = B.ncols;
+    if (l2 < l && m2 && n2)
         GF2_TRY(m4rm_view(sub_view(C, 0, 0, m2, n2), sub_view(A, 0, l2, m2, l - l2), sub_view(B, l2, 0, l - l2, n2),
                           1, s));
     if (m2 < m)
-        GF2_TRY(m4rm_view(sub_view(C, m2, 0, m - m2, n), sub_view(A, m2, 0, m - m2, l), B, accumulate, s));
+        GF2_TRY(m4rm_view(sub_view(C, m2, 0, m - m2, n), sub_view(A, m2, 0, m - m2, l), B, acc_rest, s));
     if (n2 < n)
         GF2_TRY(m4rm_view(sub_view(C, 0, n2, m2, n - n2), sub_view(A, 0, 0, m2, l), sub_view(B, 0, n2, l, n - n2),
-                          accumulate, s));
+                          acc_rest, s));
     return GF2_OK;
+}
+
+// m4rm.py:124-155 as the drop-in runs it: one base-case product (no
+// recursion) on the M4RM kernel, or on the selected tensor engine once the
+// product is past the measured crossover -- at least tensor_min_work()
+// bit-ops and every side >= tensor_min_leaf() (the M4RM kernel keeps small
+// and skinny products: cfg1 1024^3 13 us on M4RM). Engine 0 forces M4RM.
+int base_mul(const gf2_view &c, const gf2_view &a, const gf2_view &b, int accumulate, cudaStream_t s) {
+    M4rmBatch mb{a.data, a.pitch, 0, b.data, b.pitch, 0, c.data, c.pitch, 0, a.nrows, a.ncols, b.ncols, 1, accumulate};
+    const double work = (double)a.nrows * (double)a.ncols * (double)b.ncols;
+    const int64_t side = std::min(a.nrows, std::min(a.ncols, b.ncols));
+    if (g_engine == 0 || work < tensor_min_work() || side < tensor_min_leaf()) return launch_m4rm(mb, s);
+    return launch_umma(mb, g_engine - 1, s);
 }
 
 }  // namespace gf2

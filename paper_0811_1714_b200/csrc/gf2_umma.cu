@@ -306,336 +306,6 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
     }
 }
 
-// ------------------------------------------------------------------ converter-fed i8
-// k_umma_cv: the same 2-SM tcgen05 pipeline, but the operand tiles are built
-// in shared memory straight from the PACKED bits by 8 converter warps -- no
-// byte-expanded copies in HBM. Trick: with SIGNED int8 a set bit may become
-// 0xFF (= -1): (-1)(-1) = +1, so the s32 dot product still counts the common
-// ones. prmt(x << s, 0, 0xBA98) replicates bit 7 of each byte of (x << s),
-// i.e. turns 4 bits of x into 4 bytes with 2 instructions (the shift runs on
-// the FMA pipe as IMAD.SHL). The bytes come out in the order
-//     K (or N) position 4s + i  <-  element 8(3 - i) + s   (within 32)
-// A fixed permutation of K is harmless when B's rows are permuted alike
-// (row addressing only); the permutation of N is undone for free when the
-// epilogue packs parity bits (compile-time shift amounts).
-struct CvArgs {
-    const u64 *A;
-    int64_t pa, sa;
-    int64_t qoffA[4];
-    unsigned maskA[7];
-    const u64 *B;
-    int64_t pb, sb;
-    int64_t qoffB[4];
-    unsigned maskB[7];
-    int fuse;  // 1: product q = 7p + i reads XORs of source p's quadrants
-    int64_t l, Wl;
-};
-
-__device__ __forceinline__ void cp_async_8(uint32_t saddr, const void *g, bool pred) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(g), "r"(pred ? 8 : 0)
-                 : "memory");
-}
-__device__ __forceinline__ u64 lds64(uint32_t addr) {
-    u64 v;
-    asm volatile("ld.shared.u64 %0, [%1];\n" : "=l"(v) : "r"(addr));
-    return v;
-}
-
-__device__ __forceinline__ uint32_t expand4(uint32_t x, int s) {
-    uint32_t r;
-    asm("prmt.b32 %0, %1, 0, 0xBA98;\n" : "=r"(r) : "r"(x << s));
-    return r;
-}
-
-// K position of element e (0..31) in the expanded 32-block: p = 4(e & 7) + 3 - (e >> 3)
-__host__ __device__ constexpr int kpos_of(int e) { return 4 * (e & 7) + 3 - (e >> 3); }
-// element (output column) held at expanded position j (inverse of kpos_of)
-__host__ __device__ constexpr int elem_at(int j) { return 8 * (3 - (j & 3)) + (j >> 2); }
-
-constexpr int CV_THREADS = 512;
-constexpr int CV_STG = 4;                // expanded operand stages (even: steps go in pairs)
-constexpr int CV_A_ST = BM * BK;         // 16 KiB: this CTA's 128 rows x 128 K
-constexpr int CV_B_ST = (BN / 2) * BK;   // 16 KiB: this CTA's 128 columns x 128 K
-constexpr int CV_PST = 6;                // packed staging stages: 2 in use + 4 in flight
-constexpr int CV_P_ST = 256 * 8 * 8;     // 256 threads x (4 A + 4 B terms) x 8 B = 16 KiB
-constexpr int CV_SMEM = CV_STG * (CV_A_ST + CV_B_ST) + CV_PST * CV_P_ST + 2048;
-static_assert(CV_SMEM <= 232448, "k_umma_cv shared memory");
-
-__global__ void __launch_bounds__(CV_THREADS, 1) k_umma_cv(CvArgs cv, UArgs p) {
-    pdl_trigger();
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
-    const uint32_t sA = base_u32;
-    const uint32_t sB = base_u32 + CV_STG * CV_A_ST;
-    const uint32_t sP = sB + CV_STG * CV_B_ST;  // packed staging ring (cp.async)
-    const uint32_t sBar = sP + CV_PST * CV_P_ST;
-    const uint32_t bar_full = sBar, bar_empty = sBar + 8 * CV_STG, bar_tfull = sBar + 16 * CV_STG,
-                   bar_tempty = bar_tfull + 16;
-    const uint32_t tmem_holder = bar_tempty + 16;
-    const uint32_t bar_cfull = tmem_holder + 16;  // per-CTA: converter warps -> relay
-    unsigned char *gen_base = smem_raw + (base_u32 - smem_u32(smem_raw));
-    volatile uint32_t *tmem_holder_ptr = reinterpret_cast<volatile uint32_t *>(gen_base + (tmem_holder - base_u32));
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();
-    const int64_t unit = blockIdx.x >> 1, nunits = gridDim.x >> 1;
-    if (warp == 4 && lane == 0) {
-        for (int s = 0; s < CV_STG; ++s) {
-            mbar_init(bar_full + 8 * s, 2);       // one relay arrival from each CTA of the pair
-            mbar_init(bar_cfull + 8 * s, 8);      // the 8 converter warps of this CTA
-            mbar_init(bar_empty + 8 * s, 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(bar_tfull + 8 * b, 1);
-            mbar_init(bar_tempty + 8 * b, 2 * 128);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    if (warp == 5) {
-        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(tmem_holder)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
-    }
-    tc_fence_before();
-    cluster_sync();
-    tc_fence_after();
-    const uint32_t tmem_base = *tmem_holder_ptr;
-    pdl_wait();  // setup above overlapped the previous kernel's tail
-
-    const int64_t tiles = p.nprob * p.mt * p.nt;
-
-    if (warp >= 8) {
-        // ---------------- converters: packed bits -> swizzled signed bytes
-        const int ct = threadIdx.x - 256;
-        const int ra = ct >> 1, wa = ct & 1;                      // A: row, word of the K block
-        const int l8 = ct & 7, qq = ct >> 3;                      // B: conflict-free lane map
-        const int ba = l8 >> 1, wb = l8 & 1, s0 = qq & 7, g32 = qq >> 3;
-        const int kr = 32 * g32 + 8 * ba + s0;                    // packed B row in the K block
-        const int kp = 32 * g32 + kpos_of(8 * ba + s0);           // its smem row (K permutation)
-        const u64 atm = tail_mask(cv.l), btm = tail_mask(p.n);
-        // steps = (tile, K block) pairs of this pair's tiles, in MMA order;
-        // step i+3's packed words are in flight (cp.async) while step i expands.
-        // Two cursors walk the steps incrementally (tile decode only on a tile
-        // change): `ld` issues the copies, `cs` consumes them.
-        // staging is [term][thread] (8 B words): lanes touch consecutive words,
-        // so the 8-byte cp.async writes and LDS.64 reads are conflict-free
-        const uint32_t myslot = sP + ct * 8;
-        struct Cur {
-            int64_t t;
-            int kb;
-            const u64 *pA, *pB;  // this thread's A word / B word at kb = 0
-            unsigned ma, mb;
-            bool arow_ok, bword_ok;
-            bool alast_possible, blast;
-        };
-        auto tile_setup = [&](Cur &c) {
-            int64_t r = c.t;
-            const int64_t prob = r / (p.mt * p.nt);
-            r %= (p.mt * p.nt);
-            const int mtile = (int)(r / p.nt), ntile = (int)(r % p.nt);
-            const int64_t gq = p.q0 + prob;
-            const int64_t src = cv.fuse ? gq / 7 : gq;
-            c.ma = cv.fuse ? cv.maskA[gq % 7] : 1u;
-            c.mb = cv.fuse ? cv.maskB[gq % 7] : 1u;
-            const int64_t arow = (int64_t)mtile * 256 + rank * 128 + ra;
-            const int64_t bword = ((int64_t)ntile * 256 + rank * 128) / 64 + wb;
-            c.arow_ok = arow < p.m;
-            c.bword_ok = bword < p.Wn;
-            c.blast = bword == p.Wn - 1;
-            c.pA = cv.A + src * cv.sa + arow * cv.pa + wa;
-            c.pB = cv.B + src * cv.sb + (int64_t)kr * cv.pb + bword;
-        };
-        auto advance = [&](Cur &c) {
-            if (++c.kb == p.kblocks) {
-                c.kb = 0;
-                c.t += nunits;
-                if (c.t < tiles) tile_setup(c);
-            }
-        };
-        Cur ld{unit, 0, nullptr, nullptr, 0, 0, false, false, false, false};
-        if (ld.t < tiles) tile_setup(ld);
-        Cur cs = ld;
-        auto issue = [&](uint32_t pstage) {
-            if (ld.t < tiles) {
-                const int64_t aw = 2 * (int64_t)ld.kb + wa;
-                const bool aok = ld.arow_ok && aw < cv.Wl;
-                const int64_t krow = (int64_t)ld.kb * 128 + kr;
-                const bool bok = ld.bword_ok && krow < cv.l;
-                const u64 *pA = ld.pA + 2 * (int64_t)ld.kb;
-                const u64 *pB = ld.pB + (int64_t)ld.kb * 128 * cv.pb;
-                const uint32_t slot = myslot + pstage * CV_P_ST;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const bool ua = aok && (ld.ma & (1u << u)), ub = bok && (ld.mb & (1u << u));
-                    cp_async_8(slot + 2048 * u, ua ? (const void *)(pA + cv.qoffA[u]) : (const void *)cv.A, ua);
-                    cp_async_8(slot + 2048 * (4 + u), ub ? (const void *)(pB + cv.qoffB[u]) : (const void *)cv.B, ub);
-                }
-                advance(ld);
-            }
-            asm volatile("cp.async.commit_group;\n" ::: "memory");
-        };
-        // two steps per iteration: their load->expand->store chains interleave,
-        // one proxy fence and one warp sync cover both
-        for (uint32_t k = 0; k < 4; ++k) issue(k);
-        int stage = 0;
-        uint32_t phase = 0;
-        uint32_t pst = 0;  // packed stage of the first consumed step
-        auto expand_store = [&](uint32_t stg, u64 a, u64 b) {
-            const uint32_t aS = sA + stg * CV_A_ST + ra * 128;
-            const uint32_t bS = sB + stg * CV_B_ST + kp * 128;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint32_t x = (uint32_t)(a >> (32 * (1 - h)));
-                const uint32_t y = (uint32_t)(b >> (32 * (1 - h)));
-                uint32_t o[8], q[8];
-#pragma unroll
-                for (int s = 0; s < 8; ++s) {
-                    o[s] = expand4(x, s);
-                    q[s] = expand4(y, s);
-                }
-                const int ca = 4 * wa + 2 * h, cb = 4 * wb + 2 * h;
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(aS + ((ca ^ (ra & 7)) << 4)),
-                             "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]) : "memory");
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(aS + (((ca + 1) ^ (ra & 7)) << 4)),
-                             "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]) : "memory");
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(bS + ((cb ^ (kp & 7)) << 4)),
-                             "r"(q[0]), "r"(q[1]), "r"(q[2]), "r"(q[3]) : "memory");
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(bS + (((cb + 1) ^ (kp & 7)) << 4)),
-                             "r"(q[4]), "r"(q[5]), "r"(q[6]), "r"(q[7]) : "memory");
-            }
-        };
-        auto gather = [&](uint32_t ps, const Cur &c, u64 &a, u64 &b) {
-            const uint32_t slot = myslot + ps * CV_P_ST;
-            a = 0;
-            b = 0;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                a ^= lds64(slot + 2048 * u);
-                b ^= lds64(slot + 2048 * (4 + u));
-            }
-            if (2 * c.kb + wa == cv.Wl - 1) a &= atm;
-            if (c.blast) b &= btm;
-        };
-        while (cs.t < tiles) {
-            issue(pst + 4 >= CV_PST ? pst + 4 - CV_PST : pst + 4);
-            const uint32_t pst1 = pst + 1 == CV_PST ? 0 : pst + 1;
-            issue(pst1 + 4 >= CV_PST ? pst1 + 4 - CV_PST : pst1 + 4);
-            asm volatile("cp.async.wait_group 4;\n" ::: "memory");  // steps i, i+1 landed
-            u64 a0, b0, a1 = 0, b1 = 0;
-            gather(pst, cs, a0, b0);
-            Cur c1 = cs;
-            advance(c1);
-            const bool two = c1.t < tiles;
-            if (two) gather(pst1, c1, a1, b1);
-            const int stage1 = stage + 1;  // CV_STG even: a pair never wraps mid-way
-            mbar_wait(bar_empty + 8 * stage, phase ^ 1);
-            expand_store(stage, a0, b0);
-            if (two) {
-                mbar_wait(bar_empty + 8 * stage1, phase ^ 1);
-                expand_store(stage1, a1, b1);
-            }
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(bar_cfull + 8 * stage);  // CTA-scope release only
-                if (two) mbar_arrive(bar_cfull + 8 * stage1);
-            }
-            stage += 2;
-            if (stage == CV_STG) {
-                stage = 0;
-                phase ^= 1;
-            }
-            pst = pst1 + 1 == CV_PST ? 0 : pst1 + 1;
-            cs = c1;
-            if (two) advance(cs);
-        }
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    } else if (warp == 6 && lane == 0) {
-        // ---------------- relay: one cluster-scope arrive per stage and CTA
-        // (a release.cluster per converter warp costs a GPU-wide membar each)
-        int stage = 0;
-        uint32_t phase = 0;
-        for (int64_t t = unit; t < tiles; t += nunits) {
-            for (int kb = 0; kb < p.kblocks; ++kb) {
-                mbar_wait(bar_cfull + 8 * stage, phase);
-                mbar_arrive_leader(bar_full + 8 * stage);
-                if (++stage == CV_STG) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-            }
-        }
-    } else if (warp == 4 && lane == 0 && rank == 0) {
-        // ---------------- MMA issuer (leader CTA): signed int8, M=256 N=256
-        const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) |
-                               ((uint32_t)(256 >> 4) << 24);
-        int stage = 0;
-        uint32_t phase = 0;
-        int it = 0;
-        for (int64_t t = unit; t < tiles; t += nunits, ++it) {
-            const int acc = it & 1;
-            const uint32_t acc_phase = (it >> 1) & 1;
-            mbar_wait(bar_tempty + 8 * acc, acc_phase ^ 1);
-            tc_fence_after();
-            const uint32_t taddr = tmem_base + acc * BN;
-            for (int kb = 0; kb < p.kblocks; ++kb) {
-                mbar_wait(bar_full + 8 * stage, phase);
-                tc_fence_after();
-#pragma unroll
-                for (int k = 0; k < BK / 32; ++k) {
-                    const uint64_t ad = smem_desc(sA + stage * CV_A_ST + k * 32, 16, 1024);
-                    const uint64_t bd = smem_desc(sB + stage * CV_B_ST + k * 32 * 128, 16, 1024);
-                    umma_cg<0, 2>(taddr, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
-                }
-                umma_commit_cg<2>(bar_empty + 8 * stage);
-                if (++stage == CV_STG) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-            }
-            umma_commit_cg<2>(bar_tfull + 8 * acc);
-        }
-    } else if (warp < 4) {
-        // ---------------- epilogue: TMEM -> parity bits (N permutation undone) -> C
-        const int qd = warp;  // TMEM lane quadrant
-        int it = 0;
-        for (int64_t t = unit; t < tiles; t += nunits, ++it) {
-            int64_t r = t;
-            const int64_t prob = r / (p.mt * p.nt);
-            r %= (p.mt * p.nt);
-            const int mtile = (int)(r / p.nt), ntile = (int)(r % p.nt);
-            const int acc = it & 1;
-            const uint32_t acc_phase = (it >> 1) & 1;
-            mbar_wait(bar_tfull + 8 * acc, acc_phase);
-            tc_fence_after();
-            uint32_t packed[BN / 32];
-#pragma unroll
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t pk = 0;
-#pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {  // 16 columns at a time (register budget)
-                    uint32_t v[16];
-                    TMEM_LD16(tmem_base + ((uint32_t)(qd * 32) << 16) + acc * BN + c * 32 + hf * 16, v);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) pk |= (v[j] & 1u) << (31 - elem_at(16 * hf + j));
-                }
-                packed[c] = pk;
-            }
-            tc_fence_before();
-            mbar_arrive_leader(bar_tempty + 8 * acc);
-            const int64_t row = (int64_t)mtile * 256 + (int64_t)rank * BM + qd * 32 + lane;
-            store_row(p, packed, row, ntile, p.q0 + prob);
-        }
-    }
-    tc_fence_before();
-    cluster_sync();
-    if (warp == 5) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem_base) : "memory");
-    }
-}
-
 // ------------------------------------------------------------------ host
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
@@ -712,7 +382,9 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
             UmmaJob c = jb;
             c.A += s0 * jb.sa;
             c.B += s0 * jb.sb;
-            c.C += s0 * (jb.fuse_post ? 1 : per_src) * jb.sc;  // C per source (fused post) or per leaf
+            // C problems per source: with the post-addition fused, one per 7
+            // leaves (1 with one fused level, 7 with two); else one per leaf
+            c.C += s0 * (jb.fuse_post ? std::max<int64_t>(1, per_src / 7) : per_src) * jb.sc;
             c.nsrc = std::min<int64_t>(max_src, jb.nsrc - s0);
             GF2_TRY(launch_umma_job(c, kind, s));
         }
@@ -738,56 +410,6 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
                                                 Geo<2>::SMEM), "umma smem attr"));
     }
     if (kind == 2) return launch_umma_f4(jb, nprob, s);
-    // i8 with 2-SM pairs: operand tiles built in shared memory from the packed
-    // bits (k_umma_cv) -- no byte expansion pass
-    // opt-in (GF2_UMMA_CONV=1): shared-memory-bandwidth bound today, see DESIGN.md §4.4
-    static const bool conv = getenv("GF2_UMMA_CONV") && atoi(getenv("GF2_UMMA_CONV")) == 1;
-    static const int cgc = getenv("GF2_UMMA_CG") ? atoi(getenv("GF2_UMMA_CG")) : 2;
-    if (kind == 0 && conv && cgc == 2 && jb.fuse_pre <= 1) {
-        static bool cv_attr[64] = {};
-        if (first_on_device(cv_attr)) {
-            GF2_TRY(check_cuda(cudaFuncSetAttribute(k_umma_cv, cudaFuncAttributeMaxDynamicSharedMemorySize, CV_SMEM),
-                               "umma_cv smem attr"));
-        }
-        CvArgs cv{};
-        cv.A = jb.A; cv.pa = jb.pa; cv.sa = jb.sa;
-        cv.B = jb.B; cv.pb = jb.pb; cv.sb = jb.sb;
-        cv.fuse = jb.fuse_pre;
-        cv.qoffA[1] = jb.l / 64; cv.qoffA[2] = jb.m * jb.pa; cv.qoffA[3] = cv.qoffA[1] + cv.qoffA[2];
-        cv.qoffB[1] = jb.n / 64; cv.qoffB[2] = jb.l * jb.pb; cv.qoffB[3] = cv.qoffB[1] + cv.qoffB[2];
-        for (int i = 0; i < 7; ++i) {
-            cv.maskA[i] = jb.maskA[i];
-            cv.maskB[i] = jb.maskB[i];
-        }
-        cv.l = jb.l;
-        cv.Wl = words_per_row(jb.l);
-        UArgs ua{};
-        ua.C = jb.C; ua.pc = jb.pc; ua.sc = jb.sc;
-        ua.m = jb.m; ua.n = jb.n; ua.Wn = words_per_row(jb.n);
-        ua.mt = (int)((jb.m + 255) / 256);
-        ua.nt = (int)((jb.n + BN - 1) / BN);
-        ua.kblocks = (int)((jb.l + BK - 1) / BK);
-        ua.kchunk_blocks = ua.kblocks;
-        ua.nchunks = 1;
-        ua.nprob = nprob;
-        ua.q0 = 0;
-        ua.post = jb.fuse_post;
-        if (jb.fuse_post) {
-            ua.qoffC[1] = jb.n / 64; ua.qoffC[2] = jb.m * jb.pc; ua.qoffC[3] = ua.qoffC[1] + ua.qoffC[2];
-            for (int i = 0; i < 7; ++i) ua.post_mask[i] = jb.maskC[i];
-            ua.mode = 2;
-        } else {
-            ua.mode = jb.accumulate ? 1 : 0;
-        }
-        const int64_t tiles = nprob * ua.mt * ua.nt;
-        const int64_t pairs = std::min<int64_t>(tiles, num_sms() / 2);
-        const int tidx = timer_begin(s, (double)jb.m * (double)jb.l * (double)jb.n * (double)nprob);
-        int rc = check_cuda(launch_k(k_umma_cv, dim3((unsigned)(2 * pairs)), dim3(CV_THREADS), CV_SMEM, s, 2, cv, ua),
-                            "k_umma_cv launch");
-        note_launch();
-        timer_end(tidx, s);
-        return rc;
-    }
     const int64_t kp = (jb.l + 15) / 16 * 16, np = (jb.n + 15) / 16 * 16;
     // byte operands for at most ~8 GiB of problems per launch (cfg5-sized
     // recursions have thousands of leaves); chunks reuse one buffer

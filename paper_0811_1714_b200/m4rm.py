@@ -7,6 +7,13 @@ update, cache row block). They are validated exactly as the reference does
 (StripeSpec, m4rm.py:28-42); the device kernel fixes its own geometry
 (8-bit Gray tables, 4 per 32-row half stage, register-resident C tiles),
 which changes nothing in the result: the product is exact.
+
+Dispatch (gf2_mul_base): products past the measured crossover -- at least
+1e10 bit-ops with every side >= 640 -- run on the selected tensor engine
+(tcgen05 kind::mxf4 by default), which computes the same product faster
+(the reference's cfg4 call mul_m4rm_into(C, A, B, 8, 512, 8): 0.70 ms on the
+M4RM kernel, ~0.27 ms on tc-f4); smaller products, e.g. cfg1's 1024^3, run
+the M4RM kernel. set_engine("m4rm") forces the M4RM kernel everywhere.
 """
 
 from __future__ import annotations
@@ -47,8 +54,8 @@ def _validate(a: Mat, b: Mat, k: int, t: int, b_s: int) -> StripeSpec:
 
 def _mul_into(c: Mat, a: Mat, b: Mat, k: int, accumulate: bool) -> None:
     _check_cuda_dev(c, a, b)
-    _lib.check(_lib.lib_cuda().gf2_m4rm(c._view(), a._view(), b._view(),
-                                        int(k), int(accumulate), _stream()))
+    _lib.check(_lib.lib_cuda().gf2_mul_base(c._view(), a._view(), b._view(),
+                                            int(k), int(accumulate), _stream()))
 
 
 def mul_m4rm(a: Mat, b: Mat, k: int) -> BitMatrix:

@@ -55,13 +55,17 @@ class HostPipeline:
                 f"got {arr.dtype} {arr.shape}")
 
     def submit(self, a_words: np.ndarray, b_words: np.ndarray,
-               c_out: np.ndarray) -> None:
-        """Queue C = A.B; c_out is filled once `sync()` (or a later
-        `submit` that reuses this buffer set) has completed."""
+               c_out: np.ndarray, c_in: np.ndarray | None = None) -> None:
+        """Queue C = A.B -- or, with `c_in`, C = C_in + A.B (the addmul of
+        cfg4 / cfg5: C_in is uploaded with A and B and the product is XORed
+        into it); c_out is filled once `sync()` (or a later `submit` that
+        reuses this buffer set) has completed."""
         import torch
         self._check(a_words, self.m, self.l, "A")
         self._check(b_words, self.l, self.n, "B")
         self._check(c_out, self.m, self.n, "C")
+        if c_in is not None:
+            self._check(c_in, self.m, self.n, "C_in")
         k = self.i % 2
         a, b, c = self.sets[k]
         lib = _lib.lib_cuda()
@@ -73,6 +77,11 @@ class HostPipeline:
                                       a_words.strides[0] // 8, s))
             _lib.check(lib.gf2_upload(b._view(), b_words.ctypes.data,
                                       b_words.strides[0] // 8, s))
+            if c_in is not None:
+                if self.used[k]:
+                    self.h2d.wait_event(self.downloaded[k])  # set k's C read out
+                _lib.check(lib.gf2_upload(c._view(), c_in.ctypes.data,
+                                          c_in.strides[0] // 8, s))
             self.uploaded[k].record(self.h2d)
         with torch.cuda.stream(self.comp):
             self.comp.wait_event(self.uploaded[k])
@@ -80,7 +89,7 @@ class HostPipeline:
                 self.comp.wait_event(self.downloaded[k])   # set k's C read out
             _lib.check(lib.gf2_strassen(
                 c._view(), a._view(), b._view(), int(self.params.cutoff),
-                int(self.params.k), 0, self.comp.cuda_stream))
+                int(self.params.k), int(c_in is not None), self.comp.cuda_stream))
             self.computed[k].record(self.comp)
         with torch.cuda.stream(self.d2h):
             self.d2h.wait_event(self.computed[k])
@@ -135,16 +144,19 @@ class ShardedHostPipeline:
         self.i = 0
 
     def submit(self, a_words: np.ndarray, b_words: np.ndarray,
-               c_out: np.ndarray) -> None:
-        """Queue C_p = A_p . B. `a_words`: this rank's rows of A; `b_words`:
-        (l, width) with at least this rank's block of rows filled (the rest
-        is not read); `c_out` receives this rank's rows of C."""
+               c_out: np.ndarray, c_in: np.ndarray | None = None) -> None:
+        """Queue C_p = A_p . B (or, with `c_in`, C_p = C_in,p + A_p . B).
+        `a_words`: this rank's rows of A; `b_words`: (l, width) with at
+        least this rank's block of rows filled (the rest is not read);
+        `c_in` / `c_out`: this rank's rows of C."""
         import torch
         from .core import window
         from .sharded import mul_sharded
         HostPipeline._check(self, a_words, self.m, self.l, "A")
         HostPipeline._check(self, b_words, self.l, self.n, "B")
         HostPipeline._check(self, c_out, self.m, self.n, "C")
+        if c_in is not None:
+            HostPipeline._check(self, c_in, self.m, self.n, "C_in")
         k = self.i % 2
         a, b, c = self.sets[k]
         lib = _lib.lib_cuda()
@@ -158,13 +170,18 @@ class ShardedHostPipeline:
                 _lib.check(lib.gf2_upload(
                     window(b, k0, 0, k1 - k0, self.n)._view(),
                     b_words[k0:k1].ctypes.data, b_words.strides[0] // 8, s))
+            if c_in is not None:
+                if self.used[k]:
+                    self.h2d.wait_event(self.downloaded[k])  # set k's C read out
+                _lib.check(lib.gf2_upload(c._view(), c_in.ctypes.data,
+                                          c_in.strides[0] // 8, s))
             self.uploaded[k].record(self.h2d)
         with torch.cuda.stream(self.comp):
             self.comp.wait_event(self.uploaded[k])
             if self.used[k]:
                 self.comp.wait_event(self.downloaded[k])   # set k's C read out
             mul_sharded(a, b, self.params, src=None, group=self.group,
-                        npanels=self.npanels, c=c, accumulate=False)
+                        npanels=self.npanels, c=c, accumulate=c_in is not None)
             self.computed[k].record(self.comp)
         with torch.cuda.stream(self.d2h):
             self.d2h.wait_event(self.computed[k])

@@ -101,9 +101,18 @@ def mul_sharded(a_shard, b, params=None, src: int | None = 0, group=None,
     only this rank's block of rows (`owned_rows`). If `c` is given the
     product is accumulated into it (addmul) -- or overwrites it with
     accumulate=False -- else a fresh C_p is returned."""
-    from .core import create, window, zero_into
+    from .core import BitMatrix, create, window, zero_into
+    from .errors import DimensionError
     from .strassen import addmul
 
+    if not isinstance(b, BitMatrix):
+        # the broadcast moves whole rows of B's storage; a window's rows
+        # would carry (and overwrite) its parent's columns on the receivers
+        raise TypeError("mul_sharded broadcasts an owned BitMatrix B "
+                        f"(got {type(b).__name__}; copy_out a window first)")
+    if a_shard.ncols != b.nrows:
+        raise DimensionError(
+            f"inner dimensions {a_shard.ncols} and {b.nrows} differ")
     m, l, n = a_shard.nrows, a_shard.ncols, b.ncols
     if c is None:
         c = create(m, n, a_shard.device)

@@ -15,20 +15,43 @@ def pytest_configure(config):
         "markers", "slow: seconds-long CPU oracle run at config size")
 
 
+BUILD_ERRORS: dict[str, str] = {}
+
+
 def _ensure_built() -> None:
-    """Build libgf2b200.so and the oracle's C port if a fresh checkout lacks
-    them (the built files are git-ignored); nvcc cross-compiles without a GPU."""
+    """Run make for libgf2b200.so and the oracle's C port (incremental, so an
+    edited .cu is rebuilt; the built files are git-ignored and nvcc
+    cross-compiles without a GPU). A failed build (e.g. no nvcc on this
+    machine) does not abort collection: it is recorded, and the tests that
+    need that library are skipped with the reason (pytest_collection_modifyitems)."""
     import subprocess
-    lib = os.path.join(ROOT, "paper_0811_1714_b200", "libgf2b200.so")
-    port = os.path.join(ROOT, "oracle", "libgf2oracle.so")
-    if not os.path.exists(lib):
-        subprocess.run(["make", "-s", "-j4", "-C", os.path.join(ROOT, "paper_0811_1714_b200", "csrc")],
-                       check=True)
-    if not os.path.exists(port):
-        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
+    targets = {"libgf2b200": (["make", "-s", "-j8", "-C",
+                               os.path.join(ROOT, "paper_0811_1714_b200", "csrc")],
+                              os.path.join(ROOT, "paper_0811_1714_b200", "libgf2b200.so")),
+               "libgf2oracle": (["make", "-s", "-C", os.path.join(ROOT, "oracle")],
+                                os.path.join(ROOT, "oracle", "libgf2oracle.so"))}
+    for name, (cmd, out) in targets.items():
+        try:
+            subprocess.run(cmd, check=True, capture_output=True, text=True)
+        except (OSError, subprocess.CalledProcessError) as exc:
+            err = getattr(exc, "stderr", "") or str(exc)
+            if not os.path.exists(out):
+                BUILD_ERRORS[name] = f"{name} build failed: {err.strip()[-400:]}"
+            else:   # keep testing the existing build, but say it is stale
+                print(f"conftest: {name} rebuild failed, using the existing "
+                      f"{out}: {err.strip()[-400:]}", file=sys.stderr)
 
 
 _ensure_built()
+
+
+def pytest_collection_modifyitems(config, items):
+    if not BUILD_ERRORS:
+        return
+    reason = "; ".join(BUILD_ERRORS.values())
+    for item in items:
+        if "libgf2b200" in BUILD_ERRORS and item.get_closest_marker("gpu"):
+            item.add_marker(pytest.mark.skip(reason=reason))
 
 
 def has_cuda() -> bool:

@@ -157,5 +157,100 @@ def main(big: bool):
     print(json.dumps(prev, indent=1))
 
 
+def main_api():
+    """golden_api.npz: the drop-in surface beyond the multiply entries --
+    schedule_winograd with a mul_cubic stub multiplier (test_strassen.py:
+    66-111; the call order, the final C and the scratch buffers X, Y after
+    the 22 steps pin the schedule itself), peel_fixup (test_strassen.py:
+    114-160), make_table from window sources with a live right edge and a
+    narrower refill (test_graycode.py:100-137), default_params / choose_k
+    (tuning.py:29-65) and Gray codes up to k = 16 (graycode.py:38-48)."""
+    out = {}
+    # --- schedule_winograd
+    sched = [(128, 128, 128, 2, 3, 64, 64, 64), (70, 256, 128, 4, 5, 35, 128, 64),
+             (130, 384, 256, 21, 22, 65, 192, 128)]
+    for i, (m, l, n, sa, sb, m2, l2, n2) in enumerate(sched):
+        a, b = g.random(m, l, sa), g.random(l, n, sb)
+        c = g.random(m, n, 100 + i)                 # junk: every quadrant is overwritten
+        x, y = g.random(m2, max(l2, n2), 200 + i), g.random(l2, n2, 300 + i)
+        calls = []
+        names = {id(c): 0, id(x): 1, id(a): 2, id(b): 3, id(y): 4}
+
+        def mult(cc, aa, bb):
+            rec = []
+            for w in (cc, aa, bb):
+                p = w.parent if isinstance(w, g.MatrixWindow) else w
+                ro = w.row_offset if isinstance(w, g.MatrixWindow) else 0
+                co = w.col_offset if isinstance(w, g.MatrixWindow) else 0
+                rec += [names[id(p)], ro, co, w.nrows, w.ncols]
+            calls.append(rec)
+            g.copy_into(cc, g.mul_cubic(aa, bb))
+
+        g.schedule_winograd(a, b, c, (x, y), mult)
+        assert g.equal(c, g.mul_cubic(a, b))
+        out[f"sched{i}_c"] = c.words.copy()
+        out[f"sched{i}_x"] = x.words.copy()
+        out[f"sched{i}_y"] = y.words.copy()
+        out[f"sched{i}_calls"] = np.array(calls, dtype=np.int64)
+    out["sched_cases"] = np.array(sched, dtype=np.int64)
+    # --- peel_fixup: C's top-left block from the cubic product, rest junk
+    peel = [(65, 64, 64, 14, 15, 64, 64, 64), (100, 70, 130, 16, 17, 64, 64, 64),
+            (300, 300, 300, 18, 19, 256, 256, 256), (64, 64, 64, 12, 13, 64, 64, 64),
+            (200, 333, 70, 23, 24, 128, 256, 64)]
+    for i, (m, l, n, sa, sb, m2, l2, n2) in enumerate(peel):
+        a, b = g.random(m, l, sa), g.random(l, n, sb)
+        c = g.random(m, n, 400 + i)
+        g.copy_into(g.window(c, 0, 0, m2, n2),
+                    g.mul_cubic(g.window(a, 0, 0, m2, l2), g.window(b, 0, 0, l2, n2)))
+        out[f"peel{i}_before"] = c.words.copy()
+        g.peel_fixup(c, a, b, m2, l2, n2, g.MulParams(cutoff=64))
+        assert ref.first_mismatch(c, ref.naive_product(a, b)) is None
+        out[f"peel{i}_c"] = c.words.copy()
+    out["peel_cases"] = np.array(peel, dtype=np.int64)
+    # --- make_table
+    parent = g.random(6, 192, 8)
+    win = g.window(parent, 0, 64, 6, 70)
+    t = g.CombinationTable(4, 70)
+    g.make_table(win, 1, 4, t)
+    out["table_win_k4"] = t.matrix.words.copy()
+    b = g.random(8, 64, 6)
+    t = g.CombinationTable(8, 64)
+    g.make_table(b, 0, 8, t)
+    g.make_table(b, 0, 3, t)
+    out["table_refill_matrix"] = t.matrix.words.copy()       # rows 8.. keep the k=8 fill
+    pb = g.random(40, 1000, 9)
+    w = g.window(pb, 5, 128, 20, 777)
+    t = g.CombinationTable(12, 777)
+    g.make_table(w, 3, 12, t)
+    out["table_win_k12"] = t.matrix.words.copy()
+    # --- tuning rules the drop-in restates
+    kat = []
+    for l1 in (1, 4096, 32768, 49152, 1 << 20):
+        for l2 in (1 << 12, 100000, 1 << 20, 3 << 20, 50 << 20):
+            try:
+                p = g.default_params(l1, l2)
+                kat.append((l1, l2, p.cutoff, p.b_s, p.k, p.t))
+            except g.ParameterError:
+                kat.append((l1, l2, -1, -1, -1, -1))
+    out["default_params_kat"] = np.array(kat, dtype=np.int64)
+    from gf2mat.tuning import choose_k
+    ck = [(bs, l1, t, nc, choose_k(bs, l1, t, nc if nc else None))
+          for bs in (2, 3, 64, 500, 1024, 4096, 65536) for l1 in (1024, 32768)
+          for t in (1, 8) for nc in (0, 64, 2048)]
+    out["choose_k_kat"] = np.array(ck, dtype=np.int64)
+    for k in (6, 9, 12, 16):
+        gc = g.build_gray(k)
+        out[f"gray_code_k{k}"] = np.array(gc.code, dtype=np.int64)
+        out[f"gray_changed_k{k}"] = np.array(gc.changed_bit, dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, "golden_api.npz"), **out)
+    print("golden_api.npz:", len(out), "arrays")
+    # the reference's public names (gf2mat/__init__.py:62-113)
+    with open(os.path.join(HERE, "reference_api.json"), "w") as fh:
+        json.dump({"version": g.__version__, "__all__": sorted(g.__all__)}, fh, indent=1)
+
+
 if __name__ == "__main__":
-    main(big="--big" in sys.argv)
+    if "--api" in sys.argv:
+        main_api()
+    else:
+        main(big="--big" in sys.argv)

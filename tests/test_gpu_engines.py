@@ -105,7 +105,9 @@ def test_engine_switch_validation():
     assert g.get_engine() == "tc-f8"
 
 
-def test_mul_m4rm_always_runs_m4rm():
+def test_small_mul_m4rm_runs_m4rm():
+    """Below the crossover mul_m4rm is one M4RM launch on every engine
+    (large products dispatch to the tensor engine: test_gpu_api.py)."""
     g.set_engine("tc-i8")
     a, b = g.random(200, 300, 1), g.random(300, 100, 2)
     g._lib.timer_enable(True)
@@ -318,12 +320,16 @@ def test_deep_recursion_many_leaves(engine):
     assert np.array_equal(words(got), want)
 
 
-@pytest.mark.parametrize("engine", ["tc-f4", "tc-i8"])
-def test_cfg3_depth6_tensor_leaves_chunked(engine, digests):
+@pytest.mark.parametrize("engine,fuse", [("tc-f4", "1"), ("tc-i8", "1"), ("tc-f4", "2"),
+                                         ("tc-i8", "2")])
+def test_cfg3_depth6_tensor_leaves_chunked(engine, fuse, digests):
     """cfg3 at cutoff 256: depth 6, 117649 tensor-core leaves of 256^3 --
-    the tensor job runs in chunks of source problems. Leaves below 1024 go
+    the tensor job runs in chunks of source problems. Leaves below 640 go
     to M4RM by default, so GF2_TC_MIN_LEAF=256 (read once per process,
-    hence a subprocess) forces them onto the tensor engine."""
+    hence a subprocess) forces them onto the tensor engine. With
+    GF2_FUSE_LEVELS=2 each source problem feeds 49 leaves and owns 7 C
+    problems, so the chunks (<= 1337 of the 2401 sources) must advance C by
+    7 blocks per source (it advanced by one)."""
     import os
     import subprocess
     import sys
@@ -336,11 +342,50 @@ def test_cfg3_depth6_tensor_leaves_chunked(engine, digests):
         "a, b = g.random(16384, 16384, 31), g.random(16384, 16384, 32)\n"
         "print(O.digest(g.mul_strassen(a, b, g.MulParams(cutoff=256, k=8)).to_numpy()))\n"
     ) % (root, engine)
-    env = dict(os.environ, GF2_TC_MIN_LEAF="256")
+    env = dict(os.environ, GF2_TC_MIN_LEAF="256", GF2_FUSE_LEVELS=fuse)
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root,
                          capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     assert out.stdout.strip().splitlines()[-1] == digests["cfg3"]
+
+
+@pytest.mark.parametrize("engine", ["tc-i8", "tc-f8"])
+def test_single_cta_umma_tiles(engine, digests):
+    """GF2_UMMA_CG=1 (read once per process, hence a subprocess): the 8-bit
+    GEMM on single-CTA 128 x 256 tiles (tcgen05.mma.cta_group::1) instead of
+    CTA pairs -- cfg2 at cutoff 1024, cfg3, and a ragged direct addmul on
+    windows against the C port."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import paper_0811_1714_b200 as g\n"
+        "from oracle import gf2_oracle as O\n"
+        "from oracle import gf2_port as P\n"
+        "g.set_engine(%r)\n"
+        "a, b = g.random(4096, 4096, 21), g.random(4096, 4096, 22)\n"
+        "print(O.digest(g.mul_strassen(a, b, g.MulParams(cutoff=1024, k=8)).to_numpy()))\n"
+        "a, b = g.random(16384, 16384, 31), g.random(16384, 16384, 32)\n"
+        "print(O.digest(g.mul_strassen(a, b).to_numpy()))\n"
+        "pa, pb = g.random(1300, 2000, 1), g.random(1900, 1500, 2)\n"
+        "aw, bw = g.window(pa, 7, 64, 1201, 1777), g.window(pb, 3, 128, 1777, 1301)\n"
+        "c = g.random(1201, 1301, 3)\n"
+        "c0 = c.to_numpy().copy()\n"
+        "g.addmul_direct(c, aw, bw)\n"
+        "P.set_threads(P.max_threads())\n"
+        "want = P.mul_strassen(O.HostMat(1201, 1777, g.copy_out(aw).to_numpy()),\n"
+        "                      O.HostMat(1777, 1301, g.copy_out(bw).to_numpy()), cutoff=64).words\n"
+        "print(bool((c.to_numpy() == (c0 ^ want)).all()))\n"
+    ) % (root, engine)
+    out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, GF2_UMMA_CG="1"),
+                         cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = out.stdout.strip().splitlines()
+    assert lines[-3] == digests["cfg2"]
+    assert lines[-2] == digests["cfg3"]
+    assert lines[-1] == "True"
 
 
 @pytest.mark.parametrize("engine", ["tc-f4", "m4rm"])

@@ -107,6 +107,6 @@ def test_bench_reference_arm_contract():
         assert k in d, k
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
-    other = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=300,
-                           env=dict(os.environ, RANK="1", WORLD_SIZE="2"))
+    other = subprocess.run(cmd + ["--gpus", "2"], cwd=root, capture_output=True, text=True,
+                           timeout=300, env=dict(os.environ, RANK="1", WORLD_SIZE="2"))
     assert other.returncode == 0 and other.stdout == ""
