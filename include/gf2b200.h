@@ -204,6 +204,10 @@ int gf2_peel_split(int64_t m, int64_t l, int64_t n, int64_t cutoff,
  * for the bench's `gpu_launches`). */
 int64_t gf2_launch_count(void);
 
+/* Of those, the launches of the M4RM kernel (k_m4rm): tells which engine
+ * a product was dispatched to. */
+int64_t gf2_m4rm_launch_count(void);
+
 /* Kernel timer for the roofline: while enabled, every product launch (M4RM
  * or tensor-core GEMM) is bracketed by CUDA events recorded on the stream it
  * runs on. Enabling

@@ -73,6 +73,7 @@ SIGNATURES = {
     "gf2_peel_split": (ctypes.c_int, [ctypes.c_int64] * 4
                        + [ctypes.POINTER(ctypes.c_int64)]),
     "gf2_launch_count": (ctypes.c_int64, []),
+    "gf2_m4rm_launch_count": (ctypes.c_int64, []),
     "gf2_timer_enable": (ctypes.c_int, [ctypes.c_int]),
     "gf2_mul_sharded": (ctypes.c_int, [_V, _V, _V, _P, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_int64, ctypes.c_int, _P]),
@@ -162,6 +163,11 @@ def current_stream() -> int:
 
 def launch_count() -> int:
     return int(load().gf2_launch_count())
+
+
+def m4rm_launch_count() -> int:
+    """Launches of the M4RM kernel alone (which engine ran a product)."""
+    return int(load().gf2_m4rm_launch_count())
 
 
 def timer_enable(on: bool = True) -> None:

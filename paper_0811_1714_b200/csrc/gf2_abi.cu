@@ -18,6 +18,7 @@ int strassen_mul(const gf2_view &C, const gf2_view &A, const gf2_view &B, int64_
 void peel_split(int64_t m, int64_t l, int64_t n, int64_t cutoff, int64_t out[4]);
 
 std::atomic<int64_t> g_launches{0};
+std::atomic<int64_t> g_m4rm_launches{0};
 int g_engine = 3;  // tcgen05 kind::mxf4: measured fastest base case
 static thread_local std::string t_err;
 
@@ -122,6 +123,7 @@ int64_t gf2_pitch_words(int64_t ncols) {
 }
 
 int64_t gf2_launch_count(void) { return g_launches.load(); }
+int64_t gf2_m4rm_launch_count(void) { return g_m4rm_launches.load(); }
 
 int gf2_timer_enable(int on) { return timer_enable(on); }
 

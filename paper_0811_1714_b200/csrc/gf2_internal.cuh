@@ -58,6 +58,7 @@ inline bool first_on_device(bool (&flags)[64]) {
 int set_error(int code, const std::string &msg);
 int check_cuda(cudaError_t e, const char *what);
 extern std::atomic<int64_t> g_launches;
+extern std::atomic<int64_t> g_m4rm_launches;
 inline void note_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 // Programmatic dependent launch (PDL). Every library kernel is launched

@@ -3,34 +3,41 @@
 // Restates m4rm.py:77-121 (`_mul_into`) + graycode.py:108-156
 // (`make_table`) for the B200 memory hierarchy:
 //
-//   * A CTA owns a C tile of BM = 64*RPT rows x 1024 columns (16 words) and
-//     keeps it in registers for the whole K loop: each thread holds a
-//     128-bit column slice of RPT rows (8 lanes = one 128-byte row, so the
-//     4 quarter-warps of a warp cover 4 rows per instruction).
-//   * K advances two 64-bit words of A (128 rows of B) per stage. The B
-//     panel (128 rows x 1024 columns, 16 KiB) and the A column words
-//     (BM x 16 B) of the NEXT stage are prefetched (TMA, or cp.async for
-//     8-byte-aligned windows) while the current stage is consumed
-//     (double-buffered).
-//   * Each half stage (32 rows of B) builds 4 Gray-code tables of 2^8 rows
-//     x 1024 bits (4 x 32 KiB) in shared memory. Table j, slot x holds the
-//     XOR of rows i of the 8-row group with bit (7-i) of x set -- exactly
-//     the reference's big-endian CombinationTable (graycode.py:78-105).
-//     Every thread builds 32 slots of one 128-bit column slice by a
-//     Gray walk held in registers, so the build costs one 16-byte shared
-//     store per slot and no shared-memory reads beyond the 8 source rows.
-//   * Lookups: for every row, the 4 bytes of the A half-word index the 4
-//     tables (MSB-first, m4rm.py:54-66); 8 lanes read one 128-byte table row
-//     as LDS.128 -- conflict-free for any index -- and XOR it into the
-//     register accumulator.
+//   * A CTA owns a C tile of BM = 512*RPT rows x 256 columns (4 words) and
+//     keeps it in registers for the whole K loop: each thread holds whole
+//     256-bit rows (rows tid, tid+512, ...). Tall, narrow tiles amortise
+//     every table over BM rows: the table build costs 256/BM of the lookup
+//     traffic (6 % at BM = 4096).
+//   * A is first rewritten word-major (A^T at word granularity, `k_words_t`:
+//     At[word][row], the l-tail masked), so the A words of one K step for
+//     BM rows are one dense TMA box and one dense LDS.64 per 32 rows.
+//   * K advances one A word (64 rows of B) per stage. A 3-slot ring of
+//     stages (the BM A words + the 64 x 256-bit B panel, both by TMA) runs
+//     ahead of the consumers on full/empty mbarriers.
+//   * Per A half-word (32 rows of B) the CTA needs 4 Gray-code tables of 2^8
+//     slots x 256 bits. Table j, slot x holds the XOR of the rows i of its
+//     8-row group with bit (7-i) of x set -- exactly the reference's
+//     big-endian CombinationTable (graycode.py:78-105). The 4 tables of a
+//     half-word are interleaved by 32-byte bank quarter (slot x of table j
+//     at x*128 + j*32). A 3-slot ring of half-word tables is kept: half-word
+//     h+2 is built by one warp pair (rotating over the 8 pairs) while all
+//     warps look up half-word h; full/empty mbarriers instead of block
+//     barriers let a warp run up to a half-word ahead of the slowest one.
+//     A builder thread makes 32 slots of one 16-byte slice with a 5-bit
+//     Gray walk in registers (one 16-byte store per slot).
+//   * Lookups: the 4 bytes of a row's A half-word index the 4 tables
+//     (MSB-first, m4rm.py:54-66). An LDS.128 is served in 8-lane phases;
+//     in each phase the lane pairs q = 0..3 read tables (q+t)&3 -- four
+//     different bank quarters -- and the two lanes of a pair start on
+//     different 16-byte slices, so a phase hits all 8 bank octets once:
+//     one wavefront per phase, the minimum, for any table indices.
 //   * Epilogue: masked store (bits beyond the window edge preserved),
 //     XOR-accumulate, or red.global.xor for split-K (order-independent, so
 //     deterministic).
 //
 // Roofline: each lookup moves 16 B of shared memory per lane and applies 8
-// rows of B to 128 columns (1024 bit-ops / 16 B = 64 bit-ops per byte);
-// table builds add 2^8/BM of that traffic. The kernel is bound by the
-// 128 B/clk/SM shared-memory crossbar.
+// rows of B to 128 columns (1024 bit-ops / 16 B = 64 bit-ops per byte). The
+// kernel is bound by the 128 B/clk/SM shared-memory port.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -42,65 +49,67 @@ namespace gf2 {
 
 namespace {
 
-constexpr int kThreads = 512;   // 16 warps = 64 quarter-warp row groups
-constexpr int kRowGroups = kThreads / 8;
-constexpr int kTables = 4;      // 8-bit tables per half stage (32 rows of B)
-constexpr int kTabRows = 256;   // 2^8 slots
-constexpr int kTileWords = 16;  // 1024 columns per C tile
-constexpr int kRowBytes = kTileWords * 8;
-constexpr int kTableBytes = kTabRows * kRowBytes;     // 32 KiB
-constexpr int kStageWords = 2;                         // A words per stage
-constexpr int kStageRows = 64 * kStageWords;           // rows of B per stage
-constexpr int kBStageBytes = kStageRows * kRowBytes;  // 16 KiB
+constexpr int kThreads = 512;              // 16 warps = 8 builder pairs
+constexpr int kTileWords = 4;              // 256 columns per C tile
+constexpr int kTabBytes = 256 * 128;       // one half-word: 4 interleaved tables, 32 KiB
+constexpr int kNT = 3;                     // table ring (half-words)
+constexpr int kNS = 3;                     // stage ring (A words)
+constexpr int kBWordBytes = 64 * 32;       // B panel of one A word: 64 rows x 32 B
 
 template <int RPT>
-constexpr int smem_bytes() {
-    return kTables * kTableBytes + 2 * kBStageBytes + 2 * (kRowGroups * RPT) * 8 * kStageWords + 16;
+constexpr int tile_rows() {
+    return kThreads * RPT;
 }
-
-// rows per TMA box of A words (the host encodes the map with the same box)
+// DIRECT: A staged straight from A as 2-word boxes (16 B per row, the
+// stage's word is one half) instead of from the word-major copy A^T -- for
+// small products, where the extra pass and launch cost more than the
+// doubled A reads
+template <int RPT, bool DIRECT>
+constexpr int stage_bytes() {
+    return tile_rows<RPT>() * (DIRECT ? 16 : 8) + kBWordBytes;
+}
+template <int RPT, bool DIRECT>
+constexpr int smem_bytes() {
+    return kNT * kTabBytes + kNS * stage_bytes<RPT, DIRECT>() + 4 * 3 * 8;
+}
+// rows per TMA box of A^T (the host encodes the map with the same box)
 template <int RPT>
 constexpr int a_box_rows() {
-    return kRowGroups * RPT < 256 ? kRowGroups * RPT : 256;
+    return tile_rows<RPT>() < 256 ? tile_rows<RPT>() : 256;
 }
 
 struct KArgs {
-    const u64 *A;
-    int64_t pa, sa;
-    const u64 *B;
-    int64_t pb, sb;
     u64 *C;
     int64_t pc, sc;
     int64_t m, l, n;
     int64_t Wl, Wn;
-    int64_t kws;  // A words per split (even unless it is the whole row)
+    int64_t kws;  // A words per split
     int nsplit;
     int mode;  // 0 store, 1 xor, 2 atomic xor
+    u64 atm;   // tail mask of A's last word (DIRECT; A^T is masked by k_words_t)
 };
 
-// cp.async with zero-fill: copies `bytes` (0..CP) of CP and zero-fills the rest.
-template <int CP>
-__device__ __forceinline__ void cp_async(uint32_t saddr, const void *g, int bytes) {
-    if (CP == 16)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(g), "r"(bytes)
-                     : "memory");
-    else
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(g), "r"(bytes)
-                     : "memory");
-}
-__device__ __forceinline__ void mbar_init1(uint32_t bar) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar) : "memory");
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
 }
 __device__ __forceinline__ void mbar_expect(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n.reg .pred p;\nWAIT_%=:\n"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
         "@!p bra WAIT_%=;\n}\n" ::"r"(bar),
         "r"(parity)
         : "memory");
+}
+// one elected arrival per warp, after every lane's shared-memory accesses
+__device__ __forceinline__ void warp_arrive(uint32_t bar, int lane) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar);
 }
 __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, uint32_t bar) {
     asm volatile(
@@ -109,200 +118,244 @@ __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap *map, int
         "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
         : "memory");
 }
-
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-
 __device__ __forceinline__ void sts128(uint32_t addr, u64 a, u64 b) {
     asm volatile("st.shared.v2.u64 [%0], {%1, %2};\n" ::"r"(addr), "l"(a), "l"(b) : "memory");
 }
 __device__ __forceinline__ void lds128(uint32_t addr, u64 &a, u64 &b) {
     asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];\n" : "=l"(a), "=l"(b) : "r"(addr));
 }
-__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(addr));
+__device__ __forceinline__ u64 lds64(uint32_t addr) {
+    u64 v;
+    asm volatile("ld.shared.u64 %0, [%1];\n" : "=l"(v) : "r"(addr));
     return v;
 }
 
-// C tile: BM = 64*RPT rows x 1024 columns, in registers. TMA: operands are
-// 16-byte aligned with 16-byte pitches, so thread 0 stages each B panel
-// (128 rows x 16 words) and the A words (BM rows x 2 words, boxes of
-// min(BM, 256) rows)
-// with cp.async.bulk.tensor onto one mbarrier per buffer (zero fill past the
-// matrix edges); otherwise every thread issues 8-byte cp.async.
-template <int RPT, bool TMA>
+// column mask of B / C word w of a row of n columns (Wn words)
+__device__ __forceinline__ u64 col_mask(int64_t w, int64_t Wn, u64 tail) {
+    return w < Wn - 1 ? ~0ULL : (w == Wn - 1 ? tail : 0ULL);
+}
+
+// A^T at word granularity: At[p][w][r] = A[p][r][w] (last word masked to l
+// columns), rows padded to mp. 32 x 32-word tiles through shared memory.
+__global__ void __launch_bounds__(256) k_words_t(const u64 *A, int64_t pa, int64_t sa, u64 *At, int64_t mp,
+                                                 int64_t m, int64_t Wl, u64 atm) {
+    pdl_begin();
+    __shared__ u64 t[32][33];
+    const int64_t prob = blockIdx.z;
+    const int64_t r0 = (int64_t)blockIdx.x * 32, w0 = (int64_t)blockIdx.y * 32;
+    const u64 *a = A + prob * sa;
+    u64 *o = At + prob * Wl * mp;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = ty; j < 32; j += 8) {
+        const int64_t r = r0 + j, w = w0 + tx;
+        u64 v = 0;
+        if (r < m && w < Wl) {
+            v = a[r * pa + w];
+            if (w == Wl - 1) v &= atm;
+        }
+        t[j][tx] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = ty; j < 32; j += 8) {
+        const int64_t w = w0 + j, r = r0 + tx;
+        if (w < Wl && r < m) o[w * mp + r] = t[tx][j];
+    }
+}
+
+template <int RPT, bool DIRECT>
 __global__ void __launch_bounds__(kThreads, 1)
     k_m4rm(KArgs p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
-    pdl_begin();
-    constexpr int BM = kRowGroups * RPT;
+    constexpr int BM = tile_rows<RPT>();
     constexpr int kABox = a_box_rows<RPT>();
-    extern __shared__ __align__(128) unsigned char smem[];
+    constexpr int kStage = stage_bytes<RPT, DIRECT>();
+    constexpr int kABytes = BM * (DIRECT ? 16 : 8);
+    extern __shared__ __align__(1024) unsigned char smem[];
     const uint32_t s_tab = (uint32_t)__cvta_generic_to_shared(smem);
-    const uint32_t s_bst = s_tab + kTables * kTableBytes;
-    const uint32_t s_ast = s_bst + 2 * kBStageBytes;
-    const uint32_t s_bar = s_ast + 2 * BM * 16;
+    const uint32_t s_st = s_tab + kNT * kTabBytes;
+    const uint32_t s_bar = s_st + kNS * kStage;
+    const uint32_t b_tfull = s_bar, b_tempty = s_bar + 24, b_sfull = s_bar + 48, b_sempty = s_bar + 72;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    const int s = lane & 7;                       // 128-bit column slice
-    const int rg = (tid >> 5) * 4 + (lane >> 3);  // row group 0..63
+    const int warp = tid >> 5;
 
     const int64_t prob = blockIdx.z / p.nsplit;
     const int split = blockIdx.z % p.nsplit;
     const int64_t col_w0 = (int64_t)blockIdx.x * kTileWords;
     const int64_t row0 = (int64_t)blockIdx.y * BM;
-    const u64 *A = p.A + prob * p.sa;
-    const u64 *B = p.B + prob * p.sb;
     u64 *C = p.C + prob * p.sc;
 
     const int64_t kw0 = (int64_t)split * p.kws;
     const int64_t kw1 = min(kw0 + p.kws, p.Wl);
-    const u64 atm = tail_mask(p.l);
+    const int nwords = kw1 > kw0 ? (int)(kw1 - kw0) : 0;
+    const int H = 2 * nwords;  // half-words
+    const u64 ntm = tail_mask(p.n);
 
-    // masks for this thread's two B words (tail of a ragged / windowed B)
-    const int64_t wj0 = col_w0 + 2 * s;
-    const u64 bm0 = (wj0 == p.Wn - 1) ? tail_mask(p.n) : ~0ULL;
-    const u64 bm1 = (wj0 + 1 == p.Wn - 1) ? tail_mask(p.n) : ~0ULL;
-
-    // stage = A words [kw, kw+2) of BM rows and the 128 matching rows of B
-    auto load_stage = [&](int64_t kw, int buf) {
-        const uint32_t bdst = s_bst + buf * kBStageBytes;
-        if (TMA) {
-            if (tid == 0) {
-                const uint32_t bar = s_bar + 8 * buf;
-                mbar_expect(bar, kBStageBytes + BM * 16);
-                tma_3d(bdst, &tmB, (int)col_w0, (int)(kw * 64), (int)prob, bar);
-#pragma unroll
-                for (int i = 0; i < BM / kABox; ++i)
-                    tma_3d(s_ast + (buf * BM + kABox * i) * 16, &tmA, (int)kw, (int)(row0 + kABox * i), (int)prob,
-                           bar);
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < (kStageRows * kTileWords) / kThreads; ++i) {
-                const int e = tid + kThreads * i;
-                const int r = e >> 4, wd = e & 15;
-                const int64_t brow = kw * 64 + r;
-                const bool ok = (brow < p.l) && (col_w0 + wd < p.Wn);
-                const u64 *src = ok ? (B + brow * p.pb + col_w0 + wd) : B;
-                cp_async<8>(bdst + r * kRowBytes + wd * 8, src, ok ? 8 : 0);
-            }
-#pragma unroll
-            for (int i = 0; i < (2 * BM + kThreads - 1) / kThreads; ++i) {
-                const int e = tid + kThreads * i;
-                if (e < 2 * BM) {
-                    const int r = e >> 1, wd = e & 1;
-                    const bool ok = (row0 + r < p.m) && (kw + wd < kw1);
-                    const u64 *src = ok ? (A + (row0 + r) * p.pa + kw + wd) : A;
-                    cp_async<8>(s_ast + (buf * BM + r) * 16 + wd * 8, src, ok ? 8 : 0);
-                }
-            }
-            cp_async_commit();
+    if (tid == 0) {
+        for (int i = 0; i < 3; ++i) {
+            mbar_init(b_tfull + 8 * i, 2);
+            mbar_init(b_tempty + 8 * i, kThreads / 32);
+            mbar_init(b_sfull + 8 * i, 1);
+            mbar_init(b_sempty + 8 * i, kThreads / 32);
         }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    pdl_begin();
+
+    // producer (thread 0): stage of local word k -> slot k % kNS
+    auto issue = [&](int k) {
+        const uint32_t dst = s_st + (k % kNS) * kStage;
+        const uint32_t bar = b_sfull + 8 * (k % kNS);
+        mbar_expect(bar, kABytes + kBWordBytes);
+#pragma unroll
+        for (int i = 0; i < BM / kABox; ++i) {
+            if (DIRECT)  // words (kw & ~1, +1) of kABox rows
+                tma_3d(dst + i * kABox * 16, &tmA, (int)((kw0 + k) & ~int64_t(1)), (int)(row0 + i * kABox),
+                       (int)prob, bar);
+            else
+                tma_3d(dst + i * kABox * 8, &tmA, (int)(row0 + i * kABox), (int)(kw0 + k), (int)prob, bar);
+        }
+        tma_3d(dst + kABytes, &tmB, (int)col_w0, (int)((kw0 + k) * 64), (int)prob, bar);
+    };
+    if (tid == 0)
+        for (int k = 0; k < nwords && k < kNS; ++k) issue(k);
+
+    // builder role (warp pair h & 7 builds half-word h): table tj, slice bs,
+    // slots sg*32 .. sg*32+31
+    const int bt = tid & 63;
+    const int tj = (bt >> 1) & 3;
+    const int bs = bt & 1;
+    const int sg = bt >> 3;
+    const u64 bm0 = col_mask(col_w0 + 2 * bs, p.Wn, ntm);
+    const u64 bm1 = col_mask(col_w0 + 2 * bs + 1, p.Wn, ntm);
+    auto build = [&](int h) {
+        const int slot = h % kNT;
+        const int k = h >> 1;
+        if (h >= kNT) mbar_wait(b_tempty + 8 * slot, ((h - kNT) / kNT) & 1);
+        mbar_wait(b_sfull + 8 * (k % kNS), (k / kNS) & 1);
+        // rows 32*(h&1) + 8*tj + j of the word's B panel; lane tj reads row
+        // (i + tj) & 7 at step i, so the 4 tables' rows sit in 4 bank quarters
+        const uint32_t rb = s_st + (k % kNS) * kStage + kABytes + (32 * (h & 1) + 8 * tj) * 32 + bs * 16;
+        u64 c0 = 0, c1 = 0;
+        u64 x0[5], x1[5];  // slot bits 4..0 <-> rows 3..7
+#pragma unroll
+        for (int e = 0; e < 5; ++e) x0[e] = x1[e] = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int j = (i + tj) & 7;
+            u64 y0, y1;
+            lds128(rb + j * 32, y0, y1);
+            y0 &= bm0;
+            y1 &= bm1;
+            // slot bits 7..5 (= sg bits 2..0) <-> rows 0..2
+            const bool hi = (j < 3) && ((sg >> (2 - j)) & 1);
+            c0 ^= hi ? y0 : 0ULL;
+            c1 ^= hi ? y1 : 0ULL;
+#pragma unroll
+            for (int e = 0; e < 5; ++e) {
+                x0[e] = (j == 3 + e) ? y0 : x0[e];
+                x1[e] = (j == 3 + e) ? y1 : x1[e];
+            }
+        }
+        const uint32_t ts = s_tab + slot * kTabBytes + (sg * 32) * 128 + tj * 32 + bs * 16;
+        sts128(ts, c0, c1);
+#pragma unroll
+        for (int i = 1; i < 32; ++i) {
+            const int b = (i & 1) ? 0 : (i & 2) ? 1 : (i & 4) ? 2 : (i & 8) ? 3 : 4;  // flipped Gray bit
+            const int g = i ^ (i >> 1);
+            c0 ^= x0[4 - b];  // slot bit b <-> row 7-b
+            c1 ^= x1[4 - b];
+            sts128(ts + g * 128, c0, c1);
+        }
+        warp_arrive(b_tfull + 8 * slot, lane);
     };
 
-    u64 acc[RPT][2];
+    // lookup role: rows tid + 512*i; lane pair q (of each 8-lane phase of
+    // an LDS.128) reads table (q+t)&3 at step t, slice par first
+    const int q = (lane >> 1) & 3;
+    const int par = lane & 1;
+    uint32_t toff[4];
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) acc[i][0] = acc[i][1] = 0ULL;
+    for (int t = 0; t < 4; ++t) toff[t] = s_tab + (((q + t) & 3) << 5) + (par << 4);
 
-    // table-build role: table tj, slots [r0*16, r0*16+16), slice s
-    const int tj = rg >> 4, r0 = rg & 15;
+    u64 acc[RPT][4];  // [0..1]: slice par, [2..3]: slice 1-par
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0ULL;
 
-    if (TMA) {
-        if (tid == 0) {
-            mbar_init1(s_bar);
-            mbar_init1(s_bar + 8);
-            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-        }
-        __syncthreads();
-    }
-    if (kw0 < kw1) load_stage(kw0, 0);
-    int buf = 0;
-    uint32_t it = 0;
-    for (int64_t kw = kw0; kw < kw1; kw += kStageWords, buf ^= 1, ++it) {
-        if (TMA)
-            mbar_wait_parity(s_bar + 8 * buf, (it >> 1) & 1);
-        else
-            cp_async_wait_all();
-        __syncthreads();  // stage visible; previous lookups finished
-        if (kw + kStageWords < kw1) load_stage(kw + kStageWords, buf ^ 1);
-        const int nhalf = (kw + 1 < kw1) ? 4 : 2;
-        for (int hs = 0; hs < nhalf; ++hs) {
-            if (hs) __syncthreads();  // lookups of the previous half done before rebuild
-            // ---- build table tj from B rows 32hs + 8tj + (0..7), slice s
-            {
-                const uint32_t srow = s_bst + buf * kBStageBytes + (32 * hs + 8 * tj) * kRowBytes + s * 16;
-                u64 c0 = 0, c1 = 0, y0, y1;
+    const int pair = warp >> 1;
+    if (pair == 0 && H > 0) build(0);
+    if (pair == 1 && H > 1) build(1);
+
+    u64 a[RPT];
+    for (int h = 0; h < H; ++h) {
+        const int k = h >> 1;
+        if (!(h & 1)) {
+            mbar_wait(b_sfull + 8 * (k % kNS), (k / kNS) & 1);
+            if (DIRECT) {
+                const int64_t kw = kw0 + k;
+                const uint32_t sa = s_st + (k % kNS) * kStage + tid * 16 + (uint32_t)(kw & 1) * 8;
+                const u64 am = (kw == p.Wl - 1) ? p.atm : ~0ULL;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {  // slot bits 7..4 <-> source rows 0..3
-                    // only the rows in this slot group's high bits are read:
-                    // the lanes of other groups skip the load, which saves
-                    // shared-memory wavefronts (the kernel's binding resource)
-                    if (r0 & (8 >> i)) {
-                        lds128(srow + i * kRowBytes, y0, y1);
-                        c0 ^= y0 & bm0;
-                        c1 ^= y1 & bm1;
-                    }
-                }
-                u64 x0[4], x1[4];  // slot bits 3..0 <-> source rows 4..7
+                for (int i = 0; i < RPT; ++i) a[i] = lds64(sa + i * kThreads * 16) & am;
+            } else {
+                const uint32_t sa = s_st + (k % kNS) * kStage + tid * 8;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    lds128(srow + (4 + i) * kRowBytes, x0[i], x1[i]);
-                    x0[i] &= bm0;
-                    x1[i] &= bm1;
-                }
-                const uint32_t tbase = s_tab + tj * kTableBytes + (r0 * 16) * kRowBytes + s * 16;
-                sts128(tbase, c0, c1);
-#pragma unroll
-                for (int i = 1; i < 16; ++i) {
-                    const int b = (i & 1) ? 0 : (i & 2) ? 1 : (i & 4) ? 2 : 3;  // flipped Gray bit
-                    const int g = i ^ (i >> 1);
-                    c0 ^= x0[3 - b];  // slot bit b <-> source row 7-b
-                    c1 ^= x1[3 - b];
-                    sts128(tbase + g * kRowBytes, c0, c1);
-                }
+                for (int i = 0; i < RPT; ++i) a[i] = lds64(sa + i * kThreads * 8);
             }
-            __syncthreads();
-            // ---- lookups: A half-word hs of the stage (word hs/2, high half first)
-            const int64_t wcur = kw + (hs >> 1);
-            const uint32_t amask = (uint32_t)(((wcur == p.Wl - 1) ? atm : ~0ULL) >> ((hs & 1) ? 0 : 32));
-            const uint32_t aoff = s_ast + buf * BM * 16 + (hs >> 1) * 8 + ((hs & 1) ? 0 : 4);
-            const uint32_t base = s_tab + s * 16;
-#pragma unroll
-            for (int i = 0; i < RPT; ++i) {
-                const uint32_t hw = lds32(aoff + (i * kRowGroups + rg) * 16) & amask;
-                u64 v0, v1, w0, w1;
-                lds128(base + 0 * kTableBytes + ((hw >> 24) & 0xFF) * kRowBytes, v0, v1);
-                lds128(base + 1 * kTableBytes + ((hw >> 16) & 0xFF) * kRowBytes, w0, w1);
-                acc[i][0] ^= v0 ^ w0;
-                acc[i][1] ^= v1 ^ w1;
-                lds128(base + 2 * kTableBytes + ((hw >> 8) & 0xFF) * kRowBytes, v0, v1);
-                lds128(base + 3 * kTableBytes + (hw & 0xFF) * kRowBytes, w0, w1);
-                acc[i][0] ^= v0 ^ w0;
-                acc[i][1] ^= v1 ^ w1;
+            warp_arrive(b_sempty + 8 * (k % kNS), lane);
+            // refill: word k-1's slot takes word k-1+kNS once every warp has
+            // read word k-1 (its B panel was consumed by the builders before)
+            if (tid == 0 && k >= 1 && k - 1 + kNS < nwords) {
+                mbar_wait(b_sempty + 8 * ((k - 1) % kNS), ((k - 1) / kNS) & 1);
+                issue(k - 1 + kNS);
             }
         }
+        const int slot = h % kNT;
+        mbar_wait(b_tfull + 8 * slot, (h / kNT) & 1);
+        const uint32_t tb = slot * kTabBytes;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const uint32_t hw = (h & 1) ? (uint32_t)a[i] : (uint32_t)(a[i] >> 32);
+            const uint32_t r = __funnelshift_l(hw, hw, 8 * q);  // byte 3-t <-> table (q+t)&3
+#pragma unroll
+            for (int t = 0; t < 4; t += 2) {
+                const uint32_t ad0 = toff[t] + tb + (((r >> (24 - 8 * t)) & 0xFF) << 7);
+                const uint32_t ad1 = toff[t + 1] + tb + (((r >> (16 - 8 * t)) & 0xFF) << 7);
+                u64 v0, v1, v2, v3, w0, w1, w2, w3;
+                lds128(ad0, v0, v1);
+                lds128(ad0 ^ 16, v2, v3);
+                lds128(ad1, w0, w1);
+                lds128(ad1 ^ 16, w2, w3);
+                acc[i][0] ^= v0 ^ w0;
+                acc[i][1] ^= v1 ^ w1;
+                acc[i][2] ^= v2 ^ w2;
+                acc[i][3] ^= v3 ^ w3;
+            }
+        }
+        warp_arrive(b_tempty + 8 * slot, lane);
+        if (h + 2 < H && pair == ((h + 2) & 7)) build(h + 2);
     }
 
-    // ---- epilogue
-    const u64 ctm = tail_mask(p.n);
+    // ---- epilogue: words col_w0 + 2*par + {0,1} (acc 0,1), col_w0 + 2*(1-par) + {0,1} (acc 2,3)
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-        const int64_t row = row0 + i * kRowGroups + rg;
+        const int64_t row = row0 + i * kThreads + tid;
         if (row >= p.m) continue;
         u64 *crow = C + row * p.pc;
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const int64_t wi = wj0 + e;
+        for (int e = 0; e < 4; ++e) {
+            const int64_t wi = col_w0 + ((e < 2) ? 2 * par : 2 * (1 - par)) + (e & 1);
             if (wi >= p.Wn) continue;
             const u64 v = acc[i][e];
             if (p.mode == 2) {
                 if (v) atomicXor(reinterpret_cast<unsigned long long *>(crow + wi), (unsigned long long)v);
             } else if (p.mode == 1) {
                 crow[wi] ^= v;
-            } else if (wi == p.Wn - 1 && ctm != ~0ULL) {
-                crow[wi] = (crow[wi] & ~ctm) | v;
+            } else if (wi == p.Wn - 1 && ntm != ~0ULL) {
+                crow[wi] = (crow[wi] & ~ntm) | v;
             } else {
                 crow[wi] = v;
             }
@@ -310,17 +363,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-template <int RPT, bool TMA>
+template <int RPT, bool DIRECT>
 int launch_rpt(const KArgs &ka, const CUtensorMap &ta, const CUtensorMap &tb, int64_t col_tiles, int64_t row_tiles,
                int64_t zdim, cudaStream_t s) {
     static bool configured[64] = {};
-    constexpr int sm = smem_bytes<RPT>();
+    constexpr int sm = smem_bytes<RPT, DIRECT>();
     if (first_on_device(configured))
-        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_m4rm<RPT, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_m4rm<RPT, DIRECT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
                            "cudaFuncSetAttribute(k_m4rm)"));
     dim3 grid((unsigned)col_tiles, (unsigned)row_tiles, (unsigned)zdim);
-    GF2_LAUNCH(launch_k(k_m4rm<RPT, TMA>, grid, kThreads, sm, s, 1, ka, ta, tb));
+    GF2_LAUNCH(launch_k(k_m4rm<RPT, DIRECT>, grid, kThreads, sm, s, 1, ka, ta, tb));
     note_launch();
+    g_m4rm_launches.fetch_add(1, std::memory_order_relaxed);
     return check_cuda(cudaGetLastError(), "k_m4rm launch");
 }
 
@@ -415,35 +469,32 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
 
     const int64_t col_tiles = (Wn + kTileWords - 1) / kTileWords;
     const int64_t sms = num_sms();  // one CTA per SM is resident (smem-bound)
-    // Geometry from a shared-memory cost model (units: KiB of shared traffic
-    // per CTA and half stage of 32 B rows): the table build moves ~192 KiB
-    // whatever the tile height (4 tables x 256 slots x 128 B of stores plus
-    // the source rows), the lookups 34 KiB per RPT (RPT rows per thread:
-    // one 4-byte A load and four 128 B table rows per row group). A CTA runs
-    // 2 half stages per A word of its K range plus a fixed cost (launch,
-    // first stage in flight, epilogue) of about one half stage; CTAs run in
-    // waves of one per SM. A K split also costs the zeroing pass and
-    // red.xor. Large products keep RPT 16 (BM 1024) and split K only to fill
-    // waves (16384^3: 256 tiles, 4 splits, 6.92 waves); small ones
-    // (cfg1 1024^3) trade taller tiles for more CTAs with shorter K ranges.
-    int rpt = 16;
+    // Geometry from a shared-memory cost model (units: KiB of shared-memory
+    // port traffic per CTA and A word, i.e. 64 rows of B): the lookups move
+    // 128 KiB per RPT (512 threads x RPT rows x 8 tables x 32 B), the A
+    // words 8 KiB per RPT (TMA write + LDS), the table build ~82 KiB
+    // whatever the tile height (8 tables x 256 slots x 32 B of stores plus
+    // the source rows). A CTA runs its K range plus a fixed cost (launch,
+    // pipeline fill, epilogue) of about half a word; CTAs run in waves of
+    // one per SM. A K split also costs the zeroing pass and red.xor. Large
+    // products keep RPT 8 (BM 4096) and split K only to fill waves (16384^3:
+    // 256 tiles, 4 splits, 6.92 waves); small ones (cfg1 1024^3) trade
+    // taller tiles for more CTAs with shorter K ranges.
+    int rpt = 8;
     int nsplit = 1;
     int64_t kws = Wl;
     {
         double best = 0;
-        for (int r : {16, 8, 4, 2}) {
-            const int64_t rt = (b.m + kRowGroups * r - 1) / (kRowGroups * r);
+        for (int r : {8, 4, 2, 1}) {
+            const int64_t rt = (b.m + kThreads * r - 1) / (kThreads * r);
             const int64_t tiles = rt * col_tiles * b.nprob;
             for (int64_t n = 1; n <= 16 && n <= Wl; ++n) {
-                // A words per split: even, so every split starts its TMA
-                // boxes on a 16-byte boundary (a box at an odd word faults)
-                int64_t w = (Wl + n - 1) / n;
-                if (w < Wl) w = (w + 1) & ~int64_t(1);
+                const int64_t w = (Wl + n - 1) / n;
                 const int64_t ns = (Wl + w - 1) / w;  // splits actually used
                 if (ns != n) continue;
                 const int64_t ctas = tiles * ns;
                 const int64_t waves = (ctas + sms - 1) / sms;
-                const double per_cta = (2.0 * (double)w + 1.0) * (192.0 + 34.0 * r);
+                const double per_cta = ((double)w + 0.5) * (82.0 + 136.0 * r);
                 const double cost = (double)waves * per_cta * (ns > 1 ? 1.02 : 1.0);
                 if (best == 0 || cost < best * 0.999) {
                     best = cost;
@@ -458,55 +509,99 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
         // tuning override, GF2_M4RM_GEOM="rpt,nsplit" (tools/ only)
         static const char *geom = getenv("GF2_M4RM_GEOM");
         int r = 0, n = 0;
-        if (geom && sscanf(geom, "%d,%d", &r, &n) == 2 && (r == 2 || r == 4 || r == 8 || r == 16) && n >= 1 &&
+        if (geom && sscanf(geom, "%d,%d", &r, &n) == 2 && (r == 1 || r == 2 || r == 4 || r == 8) && n >= 1 &&
             n <= 16) {
             rpt = r;
             kws = (Wl + n - 1) / n;
-            if (kws < Wl) kws = (kws + 1) & ~int64_t(1);
             nsplit = (int)((Wl + kws - 1) / kws);
         }
     }
-    const int64_t row_tiles = (b.m + kRowGroups * rpt - 1) / (kRowGroups * rpt);
-    if ((int64_t)nsplit * b.nprob > 65535 || row_tiles > 65535)
+    const int64_t row_tiles = (b.m + kThreads * rpt - 1) / (kThreads * rpt);
+    if ((int64_t)nsplit * b.nprob > 65535 || row_tiles > 65535 || col_tiles > 2147483647)
         return set_error(GF2_ERR_PARAMETER, "m4rm grid too large");
+    if (b.m > 2147483647 || b.l > 2147483647 / 2)
+        return set_error(GF2_ERR_PARAMETER, "m4rm operand too large for a TMA map");
 
-    KArgs ka{b.A, b.pa, b.sa, b.B, b.pb, b.sb, b.C, b.pc, b.sc, b.m, b.l, b.n, Wl, Wn, kws, nsplit, 0};
-    if (nsplit > 1) {
-        if (!b.accumulate) GF2_TRY(zero_c());
-        ka.mode = 2;
-    } else {
-        ka.mode = b.accumulate ? 1 : 0;
+    // workspace: A^T at word granularity (rows padded to even) unless A is
+    // staged directly (small products with a 16-byte aligned A), and B
+    // copied to an aligned buffer when it is not 16-byte aligned with an
+    // even pitch
+    GF2_TRY(pool_setup());
+    const bool direct = rpt <= 4 && (uintptr_t)b.A % 16 == 0 && b.pa % 2 == 0 && (b.nprob == 1 || b.sa % 2 == 0) &&
+                        b.m * Wl * b.nprob <= (int64_t(1) << 20);
+    const int64_t mp = (b.m + 1) & ~int64_t(1);
+    const bool b_ok = ((uintptr_t)b.B % 16 == 0) && (b.pb % 2 == 0) && (b.nprob == 1 || b.sb % 2 == 0);
+    const int64_t wnp = (Wn + 1) & ~int64_t(1);
+    const int64_t at_words = direct ? 0 : b.nprob * Wl * mp;
+    const int64_t bs_words = b_ok ? 0 : b.nprob * b.l * wnp;
+    u64 *ws = nullptr;
+    if (at_words + bs_words) {
+        cudaError_t e = cudaMallocAsync((void **)&ws, (size_t)(at_words + bs_words) * 8, s);
+        if (e != cudaSuccess) return set_error(GF2_ERR_OOM, std::string("m4rm workspace: ") + cudaGetErrorString(e));
     }
-    const int64_t z = (int64_t)nsplit * b.nprob;
-    const int tidx = timer_begin(s, (double)b.m * (double)b.l * (double)b.n * (double)b.nprob);
-    bool tma = ((uintptr_t)b.A % 16 == 0) && ((uintptr_t)b.B % 16 == 0) && (b.pa % 2 == 0) && (b.pb % 2 == 0) &&
-               (b.nprob == 1 || (b.sa % 2 == 0 && b.sb % 2 == 0));
+    u64 *At = ws;
+    const u64 *Bm = b.B;
+    int64_t pb = b.pb, sb = b.sb;
+    int rc = GF2_OK;
+    if (!direct) {
+        dim3 grid((unsigned)((b.m + 31) / 32), (unsigned)((Wl + 31) / 32), (unsigned)b.nprob);
+        cudaError_t le = launch_k(k_words_t, grid, dim3(256), 0, s, 1, b.A, b.pa, b.sa, At, mp, b.m, Wl,
+                                  tail_mask(b.l));
+        if (le != cudaSuccess) rc = check_cuda(le, "k_words_t launch");
+        else note_launch();
+    }
+    if (rc == GF2_OK && !b_ok) {
+        u64 *Bs = ws + at_words;
+        for (int64_t q = 0; q < b.nprob && rc == GF2_OK; ++q) {
+            gf2_view dst{Bs + q * b.l * wnp, wnp, b.l, b.n};
+            gf2_view src{const_cast<u64 *>(b.B + q * b.sb), b.pb, b.l, b.n};
+            rc = launch_ewise(dst, &src, nullptr, 1, s);
+        }
+        Bm = Bs;
+        pb = wnp;
+        sb = b.l * wnp;
+    }
     CUtensorMap ta{}, tb{};
-    if (tma) {
-        // words x rows x problems; the problem stride is unused when nprob == 1
-        const uint64_t da[3] = {(uint64_t)Wl, (uint64_t)b.m, (uint64_t)b.nprob};
-        const uint64_t sa[2] = {(uint64_t)b.pa * 8, (uint64_t)(b.nprob > 1 ? b.sa : b.m * b.pa) * 8};
-        const uint32_t ba[3] = {2, (uint32_t)std::min(kRowGroups * rpt, 256), 1};
+    if (rc == GF2_OK) {
+        // A^T: rows x words x problems (DIRECT, A: words x rows x problems);
+        // B: words x rows x problems
+        const uint32_t abox = (uint32_t)std::min(kThreads * rpt, 256);
+        const uint64_t da[3] = {(uint64_t)(direct ? Wl : b.m), (uint64_t)(direct ? b.m : Wl), (uint64_t)b.nprob};
+        const uint64_t sa[2] = {(uint64_t)(direct ? b.pa : mp) * 8,
+                                (uint64_t)(direct ? (b.nprob > 1 ? b.sa : b.m * b.pa) : Wl * mp) * 8};
+        const uint32_t ba[3] = {direct ? 2u : abox, direct ? abox : 1u, 1};
         const uint64_t db[3] = {(uint64_t)Wn, (uint64_t)b.l, (uint64_t)b.nprob};
-        const uint64_t sb[2] = {(uint64_t)b.pb * 8, (uint64_t)(b.nprob > 1 ? b.sb : b.l * b.pb) * 8};
-        const uint32_t bb[3] = {(uint32_t)kTileWords, (uint32_t)kStageRows, 1};
-        tma = encode_map_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT64, (void *)b.A, da, sa, ba, false) == GF2_OK &&
-              encode_map_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT64, (void *)b.B, db, sb, bb, false) == GF2_OK;
+        const uint64_t sbb[2] = {(uint64_t)pb * 8, (uint64_t)(b.nprob > 1 ? sb : b.l * pb) * 8};
+        const uint32_t bb[3] = {(uint32_t)kTileWords, 64, 1};
+        rc = encode_map_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT64, direct ? (void *)b.A : (void *)At, da, sa, ba, false);
+        if (rc == GF2_OK) rc = encode_map_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT64, (void *)Bm, db, sbb, bb, false);
     }
-    int rc;
-    if (rpt == 16)
-        rc = tma ? launch_rpt<16, true>(ka, ta, tb, col_tiles, row_tiles, z, s)
-                 : launch_rpt<16, false>(ka, ta, tb, col_tiles, row_tiles, z, s);
-    else if (rpt == 8)
-        rc = tma ? launch_rpt<8, true>(ka, ta, tb, col_tiles, row_tiles, z, s)
-                 : launch_rpt<8, false>(ka, ta, tb, col_tiles, row_tiles, z, s);
-    else if (rpt == 4)
-        rc = tma ? launch_rpt<4, true>(ka, ta, tb, col_tiles, row_tiles, z, s)
-                 : launch_rpt<4, false>(ka, ta, tb, col_tiles, row_tiles, z, s);
-    else
-        rc = tma ? launch_rpt<2, true>(ka, ta, tb, col_tiles, row_tiles, z, s)
-                 : launch_rpt<2, false>(ka, ta, tb, col_tiles, row_tiles, z, s);
-    timer_end(tidx, s);
+    KArgs ka{b.C, b.pc, b.sc, b.m, b.l, b.n, Wl, Wn, kws, nsplit, 0, tail_mask(b.l)};
+    if (rc == GF2_OK) {
+        if (nsplit > 1) {
+            if (!b.accumulate) rc = zero_c();
+            ka.mode = 2;
+        } else {
+            ka.mode = b.accumulate ? 1 : 0;
+        }
+    }
+    if (rc == GF2_OK) {
+        const int64_t z = (int64_t)nsplit * b.nprob;
+        const int tidx = timer_begin(s, (double)b.m * (double)b.l * (double)b.n * (double)b.nprob);
+        if (rpt == 8)
+            rc = launch_rpt<8, false>(ka, ta, tb, col_tiles, row_tiles, z, s);
+        else if (rpt == 4)
+            rc = direct ? launch_rpt<4, true>(ka, ta, tb, col_tiles, row_tiles, z, s)
+                        : launch_rpt<4, false>(ka, ta, tb, col_tiles, row_tiles, z, s);
+        else if (rpt == 2)
+            rc = direct ? launch_rpt<2, true>(ka, ta, tb, col_tiles, row_tiles, z, s)
+                        : launch_rpt<2, false>(ka, ta, tb, col_tiles, row_tiles, z, s);
+        else
+            rc = direct ? launch_rpt<1, true>(ka, ta, tb, col_tiles, row_tiles, z, s)
+                        : launch_rpt<1, false>(ka, ta, tb, col_tiles, row_tiles, z, s);
+        timer_end(tidx, s);
+    }
+    if (ws) cudaFreeAsync(ws, s);
     return rc;
 }
 

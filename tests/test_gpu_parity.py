@@ -365,7 +365,7 @@ for (m, l, n, seed) in [(1000, 1100, 1300, 1), (130, 2049, 777, 2), (2100, 640, 
     if not np.array_equal(g.mul_m4rm(a, b, 8).to_numpy(), want):
         bad.append(("aligned", m, l, n))
     # odd word offsets: 8-byte staging instead of TMA
-    big_a, big_b = g.random(m + 3, l + 64, seed + 7), g.random(l + 5, n + 128, seed + 8)
+    big_a, big_b = g.random(m + 3, l + 128, seed + 7), g.random(l + 5, n + 128, seed + 8)
     aw, bw = g.window(big_a, 3, 64, m, l), g.window(big_b, 5, 64, l, n)
     ha, hb = big_a.to_numpy(), big_b.to_numpy()
     wa = O.HostMat(m, l, np.ascontiguousarray(ha[3:3 + m, 1:1 + O.words_per_row(l)]))
@@ -378,17 +378,28 @@ for (m, l, n, seed) in [(1000, 1100, 1300, 1), (130, 2049, 777, 2), (2100, 640, 
     g.mul_m4rm_into(c, aw, bw, 8)
     if not np.array_equal(c.to_numpy(), c0 ^ want_w):
         bad.append(("window-accumulate", m, l, n))
+    # mixed staging: A 16-byte aligned (TMA) with B at an odd word (8-byte
+    # B loads), and A at an odd word with B aligned (16-byte B loads)
+    aw2, bw2 = g.window(big_a, 3, 128, m, l), g.window(big_b, 5, 128, l, n)
+    wa2 = O.HostMat(m, l, np.ascontiguousarray(ha[3:3 + m, 2:2 + O.words_per_row(l)]))
+    wb2 = O.HostMat(l, n, np.ascontiguousarray(hb[5:5 + l, 2:2 + O.words_per_row(n)]))
+    wa2.words[:, -1] &= np.uint64(O.tail_mask(l))
+    wb2.words[:, -1] &= np.uint64(O.tail_mask(n))
+    if not np.array_equal(g.mul_m4rm(aw2, bw, 8).to_numpy(), P.mul_strassen(wa2, wb, cutoff=1 << 20).words):
+        bad.append(("tma-a/odd-b", m, l, n))
+    if not np.array_equal(g.mul_m4rm(aw, bw2, 8).to_numpy(), P.mul_strassen(wa, wb2, cutoff=1 << 20).words):
+        bad.append(("odd-a/aligned-b", m, l, n))
 print("BAD", bad)
 """
 
 
-@pytest.mark.parametrize("geom", ["16,1", "16,3", "8,5", "4,16", "2,8", "2,16"])
+@pytest.mark.parametrize("geom", ["8,1", "8,3", "4,5", "2,16", "1,8", "1,16"])
 def test_m4rm_every_geometry(geom):
-    """Every k_m4rm tile height (RPT 16/8/4/2 -> 1024/512/256/128 rows) and
+    """Every k_m4rm tile height (RPT 8/4/2/1 -> 4096/2048/1024/512 rows) and
     K-split count, forced through GF2_M4RM_GEOM (read once per process,
     hence a subprocess), on ragged shapes with the TMA path (aligned
-    operands) and the 8-byte cp.async path (odd word offsets), plain and
-    accumulating, against the C port."""
+    operands), the 8-byte cp.async path (odd word offsets) and both mixes,
+    plain and accumulating, against the C port."""
     import os
     import subprocess
     import sys
