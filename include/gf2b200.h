@@ -204,6 +204,12 @@ int gf2_peel_split(int64_t m, int64_t l, int64_t n, int64_t cutoff,
  * for the bench's `gpu_launches`). */
 int64_t gf2_launch_count(void);
 
+/* High-water mark (bytes) of the library's workspace in the device's
+ * stream-ordered pool since the last reset (reset = 1 restarts it at the
+ * current use): the device analogue of the reference CLI's peak_mem_bytes
+ * (counters.py peak_live_words, cli.py:161-166). */
+int gf2_workspace_peak(int64_t *bytes, int reset);
+
 /* Of those, the launches of the M4RM kernel (k_m4rm): tells which engine
  * a product was dispatched to. */
 int64_t gf2_m4rm_launch_count(void);

@@ -74,6 +74,7 @@ SIGNATURES = {
                        + [ctypes.POINTER(ctypes.c_int64)]),
     "gf2_launch_count": (ctypes.c_int64, []),
     "gf2_m4rm_launch_count": (ctypes.c_int64, []),
+    "gf2_workspace_peak": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int64), ctypes.c_int]),
     "gf2_timer_enable": (ctypes.c_int, [ctypes.c_int]),
     "gf2_mul_sharded": (ctypes.c_int, [_V, _V, _V, _P, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_int64, ctypes.c_int, _P]),
@@ -168,6 +169,14 @@ def launch_count() -> int:
 def m4rm_launch_count() -> int:
     """Launches of the M4RM kernel alone (which engine ran a product)."""
     return int(load().gf2_m4rm_launch_count())
+
+
+def workspace_peak(reset: bool = False) -> int:
+    """Bytes: high-water mark of the library's pooled device workspace
+    since the last reset (reset=True restarts it at the current use)."""
+    v = ctypes.c_int64()
+    check(load().gf2_workspace_peak(ctypes.byref(v), int(reset)))
+    return int(v.value)
 
 
 def timer_enable(on: bool = True) -> None:

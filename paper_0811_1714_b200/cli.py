@@ -9,17 +9,23 @@
 Subcommands, flags, algorithm names, CSV columns and exit codes follow the
 reference CLI (cli.py:65-351): algorithms cubic, m4rm, m4rm-blocked,
 m4rm-t<t> (t = 1..8), strassen, auto; `check` exits 1 on a mismatch, file /
-dimension errors exit 2. Added: --engine (m4rm | tc-i8 | tc-f8 | tc-f4) selects the
-Strassen leaf engine. `check` cross-checks every variant against the
-device cubic product (the reference additionally uses its CPU oracle, which
-this package deliberately does not import).
+dimension errors exit 2; `bench` writes the reference's CSV header exactly
+(cli.py:97-129, so gf2mat's parse_csv reads it), peak_mem_bytes being the
+device memory high-water mark of the timed repetitions. Added: --engine
+(m4rm | tc-i8 | tc-f8 | tc-f4) selects the Strassen leaf engine. `check`
+does what the reference's does (cli.py:181-211): a host-side naive product
+is the oracle (the reference's `_reference.naive_product`, restated here as
+a NumPy float64 matrix product mod 2 -- the checker, never a compute path),
+the device cubic product is checked against it, and every variant is
+compared with the oracle and then with the cubic product.
 """
 
 from __future__ import annotations
 
 import argparse
-import csv
 import sys
+
+import numpy as np
 
 from . import _lib
 from .core import first_difference, random
@@ -32,7 +38,7 @@ from .structure import mul_cubic
 ALGOS = ("cubic", "m4rm", "m4rm-blocked", "m4rm-t2", "m4rm-t8", "strassen",
          "auto")
 FIELDS = ("algorithm", "m", "l", "n", "k", "t", "bs", "cutoff", "reps",
-          "wall_s", "mean_s", "min_s", "engine")
+          "wall_s", "mean_s", "min_s", "peak_mem_bytes")  # cli.py:97-129 BenchRecord
 
 
 def _dims(text: str, parts: int):
@@ -80,9 +86,17 @@ def _params(args) -> MulParams:
 
 
 def _time(fn, a, b, reps):
+    """(per-repetition seconds, peak bytes): CUDA events around each call,
+    warm-up excluded (cli.py:159); the peak is the device memory high-water
+    mark of the timed repetitions above what was live before them -- torch's
+    allocations (matrices) plus the library's pooled workspace -- the
+    device analogue of counters.peak_live_words (cli.py:161-166)."""
     import torch
-    fn(a, b)                       # warm-up, excluded (cli.py:159)
+    fn(a, b)
     torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    ws0 = _lib.workspace_peak(reset=True)
     times = []
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -91,25 +105,62 @@ def _time(fn, a, b, reps):
         e1.record()
         e1.synchronize()
         times.append(e0.elapsed_time(e1) * 1e-3)
-    return times
+    peak = max(torch.cuda.max_memory_allocated() - base, 0) + max(_lib.workspace_peak() - ws0, 0)
+    return times, peak
+
+
+def _host_dense(m) -> np.ndarray:
+    """Downloaded words -> (nrows, ncols) 0/1 array (MSB-first, core.py:405-414)."""
+    w = m.to_numpy()
+    if not w.size:
+        return np.zeros((m.nrows, m.ncols), dtype=np.uint8)
+    bits = np.unpackbits(w.astype(">u8").view(np.uint8).reshape(m.nrows, -1), axis=1)
+    return bits[:, :m.ncols]
+
+
+def naive_product(a, b) -> np.ndarray:
+    """The check oracle (the reference's _reference.naive_product): the
+    product of the downloaded operands as a float64 matrix product mod 2 --
+    exact while inner dimensions stay below 2^53."""
+    da, db = _host_dense(a).astype(np.float64), _host_dense(b).astype(np.float64)
+    return (np.rint(da @ db).astype(np.int64) & 1).astype(np.uint8)
+
+
+def _first_mismatch(m, dense):
+    """First (row, col) where device matrix m differs from a 0/1 array, or None."""
+    got = _host_dense(m)
+    diff = np.argwhere(got != dense)
+    return None if not len(diff) else (int(diff[0][0]), int(diff[0][1]))
 
 
 def cmd_check(args, params) -> int:
     status = 0
+    algos = args.algo or [x for x in ALGOS if x != "cubic"]
+    col = max(len(x) for x in algos) + 2
     for m, l, n in args.dims:
         a, b = random(m, l, args.seed), random(l, n, args.seed + 1)
+        oracle = naive_product(a, b)
         ref = mul_cubic(a, b)
+        where = _first_mismatch(ref, oracle)
+        if where is not None:
+            print(f"{m}x{l}x{n}  cubic: FAIL at {where} (vs oracle)")
+            status = 1
         cells = []
-        for idx, name in enumerate(args.algo or [x for x in ALGOS if x != "cubic"]):
+        for idx, name in enumerate(algos):
             got = algorithm(name, params)(a, b)
             if args.inject_fault and idx == 0 and m and n:
                 from .core import copy_into, from_dense, to_dense, window
                 d = to_dense(window(got, 0, 0, 1, 1))
                 d[0, 0] ^= 1
                 copy_into(window(got, 0, 0, 1, 1), from_dense(d))
-            where = first_difference(got, ref)
-            cells.append(f"{name}:ok" if where is None else f"{name}:FAIL{where}")
-            status |= where is not None
+            where = _first_mismatch(got, oracle)
+            if where is None:
+                where = first_difference(got, ref)
+            if where is None:
+                cells.append(f"{name}:ok".ljust(col + 3))
+            else:
+                cells.append(f"{name}:FAIL{where}".ljust(col + 12))
+                status = 1
         print(f"{m}x{l}x{n}  " + " ".join(cells))
     print("check:", "FAIL" if status else "PASS")
     return 1 if status else 0
@@ -120,16 +171,18 @@ def cmd_bench(args, params) -> int:
     for m, l, n in args.dims or [(d, d, d) for d in (1024, 2048, 4096, 8192, 16384)]:
         a, b = random(m, l, args.seed), random(l, n, args.seed + 1)
         for name in args.algo or ["m4rm", "strassen"]:
-            ts = _time(algorithm(name, params), a, b, args.reps)
+            ts, peak = _time(algorithm(name, params), a, b, args.reps)
             rows.append({"algorithm": name, "m": m, "l": l, "n": n,
                          "k": params.k, "t": params.t, "bs": params.b_s,
                          "cutoff": params.cutoff, "reps": args.reps,
                          "wall_s": sum(ts), "mean_s": sum(ts) / len(ts),
-                         "min_s": min(ts), "engine": _lib.get_engine()})
-    fh = open(args.out, "w", newline="") if args.out else sys.stdout
-    w = csv.DictWriter(fh, fieldnames=FIELDS)
-    w.writeheader()
-    w.writerows(rows)
+                         "min_s": min(ts), "peak_mem_bytes": peak})
+    print(f"engine={_lib.get_engine()}", file=sys.stderr)
+    fh = open(args.out, "w", encoding="utf-8") if args.out else sys.stdout
+    # the reference's emit_csv format (cli.py:117-122): floats as repr
+    fh.write(",".join(FIELDS) + "\n")
+    for r in rows:
+        fh.write(",".join(repr(r[f]) if isinstance(r[f], float) else str(r[f]) for f in FIELDS) + "\n")
     if args.out:
         fh.close()
     return 0

@@ -125,6 +125,22 @@ int64_t gf2_pitch_words(int64_t ncols) {
 int64_t gf2_launch_count(void) { return g_launches.load(); }
 int64_t gf2_m4rm_launch_count(void) { return g_m4rm_launches.load(); }
 
+int gf2_workspace_peak(int64_t *bytes, int reset) {
+    GF2_TRY(pool_setup());
+    int dev = 0;
+    GF2_TRY(check_cuda(cudaGetDevice(&dev), "cudaGetDevice"));
+    cudaMemPool_t pool;
+    GF2_TRY(check_cuda(cudaDeviceGetDefaultMemPool(&pool, dev), "cudaDeviceGetDefaultMemPool"));
+    if (reset) {
+        uint64_t zero = 0;
+        GF2_TRY(check_cuda(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero), "reset pool peak"));
+    }
+    uint64_t hi = 0;
+    GF2_TRY(check_cuda(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &hi), "pool peak"));
+    if (bytes) *bytes = (int64_t)hi;
+    return GF2_OK;
+}
+
 int gf2_timer_enable(int on) { return timer_enable(on); }
 
 int gf2_set_engine(int engine) {

@@ -33,6 +33,20 @@ def test_gen_mul_roundtrip(tmp_path, capsys, golden):
         assert g.equal(g.load(c), want)
 
 
+def test_check_oracle_is_host_naive_product():
+    """check's oracle is a host product of the downloaded operands,
+    independent of every device kernel (cli.py:181-211 uses
+    _reference.naive_product the same way)."""
+    from paper_0811_1714_b200 import cli
+    a, b = g.random(70, 130, 1), g.random(130, 90, 2)
+    want = cli.naive_product(a, b)
+    assert np.array_equal(g.to_dense(g.mul_cubic(a, b)), want)
+    assert cli._first_mismatch(g.mul_strassen(a, b), want) is None
+    bad = want.copy()
+    bad[3, 77] ^= 1
+    assert cli._first_mismatch(g.mul_strassen(a, b), bad) == (3, 77)
+
+
 def test_check_pass_and_fault(capsys):
     assert run("check", "--dims", "300x200x100", "--dims", "65x64x1") == 0
     assert "check: PASS" in capsys.readouterr().out
@@ -44,9 +58,13 @@ def test_bench_csv_and_errors(tmp_path, capsys):
     out = tmp_path / "b.csv"
     assert run("bench", "--dims", "1024x1024x1024", "--reps", "2",
                "--algo", "m4rm", "--algo", "strassen", "--out", str(out)) == 0
+    # the reference's BenchRecord header, byte for byte (cli.py:97-129)
+    assert open(out).readline().strip() == ("algorithm,m,l,n,k,t,bs,cutoff,reps,wall_s,mean_s,"
+                                            "min_s,peak_mem_bytes")
     rows = list(csv.DictReader(open(out)))
     assert [r["algorithm"] for r in rows] == ["m4rm", "strassen"]
     assert all(float(r["min_s"]) <= float(r["mean_s"]) for r in rows)
+    assert all(int(r["peak_mem_bytes"]) > 0 for r in rows)  # each rep allocates its product
     assert run("mul", str(tmp_path / "missing"), str(out), str(out)) == 2
     assert run("check", "--dims", "2x2x2", "--algo", "nope") == 2
     prev = g.get_engine()
