@@ -178,6 +178,12 @@ int gf2_strassen(const gf2_view *c, const gf2_view *a, const gf2_view *b,
 typedef struct gf2_plan gf2_plan;
 int gf2_plan_strassen(gf2_plan **out, const gf2_view *c, const gf2_view *a, const gf2_view *b, int64_t cutoff,
                       int k, int accumulate);
+/* m4rm.py:124-155 `mul_m4rm*` / `mul_m4rm_into` (gf2_mul_base semantics,
+ * accumulate = 1 for C ^= A.B) captured the same way: a small product's
+ * whole host path (validation, geometry, tensor maps, 1-3 launches) becomes
+ * one graph launch. */
+int gf2_plan_m4rm(gf2_plan **out, const gf2_view *c, const gf2_view *a, const gf2_view *b, int k,
+                  int accumulate);
 int gf2_plan_launch(gf2_plan *plan, void *stream);
 int gf2_plan_destroy(gf2_plan *plan);
 

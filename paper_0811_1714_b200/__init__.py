@@ -18,7 +18,7 @@ from .core import (BitMatrix, HostMatrix, MatrixWindow, add, add_into,
                    zero_into)
 from .errors import (AlignmentError, DimensionError, FormatError, GF2MatError,
                      ParameterError)
-from .m4rm import (StripeSpec, mul_m4rm, mul_m4rm_blocked, mul_m4rm_into,
+from .m4rm import (M4rmPlan, StripeSpec, mul_m4rm, mul_m4rm_blocked, mul_m4rm_into,
                    mul_m4rm_multitable)
 from .gf2m import load, save
 from .graycode import CombinationTable, GrayCode, build_gray, make_table
@@ -45,5 +45,5 @@ __all__ = [
     "to_numpy", "trailing_bits_clean", "window", "words_per_row", "zero_into",
     "augment", "load", "mul_cubic", "save", "stack", "transpose",
     "CombinationTable", "GrayCode", "build_gray", "make_table", "choose_k",
-    "peel_fixup", "schedule_winograd", "random_into",
+    "peel_fixup", "schedule_winograd", "random_into", "M4rmPlan",
 ]

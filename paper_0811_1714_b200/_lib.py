@@ -68,6 +68,8 @@ SIGNATURES = {
                                     ctypes.c_int, _P]),
     "gf2_plan_strassen": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), _V, _V, _V,
                                          ctypes.c_int64, ctypes.c_int, ctypes.c_int]),
+    "gf2_plan_m4rm": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), _V, _V, _V,
+                                     ctypes.c_int, ctypes.c_int]),
     "gf2_plan_launch": (ctypes.c_int, [_P, _P]),
     "gf2_plan_destroy": (ctypes.c_int, [_P]),
     "gf2_peel_split": (ctypes.c_int, [ctypes.c_int64] * 4

@@ -65,14 +65,23 @@ class BitMatrix:
         self.pitch = int(lib.gf2_pitch_words(ncols))
         if device is None:
             device = torch.cuda.current_device()  # index on the current device
-        if _overwritten and self.pitch == self.width and ncols % 64 == 0:
-            # a product target whose every word the kernels overwrite whole
-            # (no padding words, no partial last word to merge into): no fill
-            self.storage = torch.empty((self.nrows, self.pitch),
-                                       dtype=torch.int64, device=device)
-        else:
-            self.storage = torch.zeros((self.nrows, self.pitch),
-                                       dtype=torch.int64, device=device)
+        self.storage = torch.empty((self.nrows, self.pitch),
+                                   dtype=torch.int64, device=device)
+        # zero-filled (core.py:176-178) by the library (a 2-D memset, no
+        # kernel): the whole pitch, or for a product target -- whose words
+        # the kernels overwrite, merging into a ragged last word -- only
+        # that last word and the padding words after it
+        first = 0
+        if _overwritten:
+            first = self.width - 1 if ncols % 64 else self.width
+        if first < self.pitch and self.nrows:
+            z = _lib.Gf2View(self.storage.data_ptr() + 8 * first, self.pitch,
+                             self.nrows, (self.pitch - first) * WORD_BITS)
+            if self.storage.get_device() == _current_device():
+                _lib.check(lib.gf2_zero(z, _stream()))
+            else:
+                with torch.cuda.device(self.storage.device):
+                    _lib.check(lib.gf2_zero(z, _lib.current_stream()))
 
     # reference-compatible accessors
     @property

@@ -82,6 +82,36 @@ static int check_same_shape(const gf2_view *out, const gf2_view *a, const char *
     return GF2_OK;
 }
 
+// capture `body(stream)` into a graph on a private stream
+template <typename F>
+int capture_plan(cudaGraph_t *g_out, cudaGraphExec_t *e_out, F body) {
+    GF2_TRY(pool_setup());
+    SideStream *sd = nullptr;
+    GF2_TRY(side_stream(&sd));  // created outside the capture
+    cudaStream_t cs = nullptr;
+    GF2_TRY(check_cuda(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "plan stream"));
+    // relaxed: the library's one-time lazy setup (function attributes,
+    // driver entry point) may run while capturing
+    int rc = check_cuda(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed), "begin capture");
+    cudaGraph_t graph = nullptr;
+    if (rc == GF2_OK) {
+        rc = body(cs);
+        const cudaError_t e = cudaStreamEndCapture(cs, &graph);
+        if (rc == GF2_OK) rc = check_cuda(e, "end capture");
+    }
+    cudaGraphExec_t exec = nullptr;
+    if (rc == GF2_OK) rc = check_cuda(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
+    cudaStreamDestroy(cs);
+    if (rc != GF2_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        return rc;
+    }
+    *g_out = graph;
+    *e_out = exec;
+    return GF2_OK;
+}
+
 }  // namespace gf2
 
 using namespace gf2;
@@ -214,7 +244,7 @@ int gf2_download(const gf2_view *src, uint64_t *host, int64_t host_stride, void 
 
 int gf2_zero(const gf2_view *dst, void *stream) {
     GF2_TRY(check_view(dst, "dst"));
-    return launch_ewise(*dst, nullptr, nullptr, 0, (cudaStream_t)stream);
+    return launch_zero(*dst, (cudaStream_t)stream);  // 2-D memset unless the right edge is ragged
 }
 
 int gf2_random(const gf2_view *dst, uint64_t seed, int64_t row_base, void *stream) {
@@ -312,29 +342,22 @@ int gf2_plan_strassen(gf2_plan **out, const gf2_view *c, const gf2_view *a, cons
     if (cutoff < 64) return set_error(GF2_ERR_PARAMETER, "cutoff " + std::to_string(cutoff) + " < 64");
     if (k < 0 || k > 16) return set_error(GF2_ERR_PARAMETER, "k=" + std::to_string(k) + " outside 0..16");
     GF2_TRY(check_mul(c, a, b));
-    GF2_TRY(pool_setup());
-    SideStream *sd = nullptr;
-    GF2_TRY(side_stream(&sd));  // created outside the capture
-    cudaStream_t cs = nullptr;
-    GF2_TRY(check_cuda(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "plan stream"));
-    // relaxed: the library's one-time lazy setup (function attributes,
-    // driver entry point) may run while capturing
-    int rc = check_cuda(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed), "begin capture");
-    cudaGraph_t graph = nullptr;
-    if (rc == GF2_OK) {
-        rc = strassen_mul(*c, *a, *b, cutoff, accumulate ? 1 : 0, cs);
-        const cudaError_t e = cudaStreamEndCapture(cs, &graph);
-        if (rc == GF2_OK) rc = check_cuda(e, "end capture");
-    }
-    cudaGraphExec_t exec = nullptr;
-    if (rc == GF2_OK) rc = check_cuda(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
-    cudaStreamDestroy(cs);
-    if (rc != GF2_OK) {
-        if (graph) cudaGraphDestroy(graph);
-        cudaGetLastError();
-        return rc;
-    }
-    *out = new gf2_plan{graph, exec};
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t e = nullptr;
+    GF2_TRY(capture_plan(&g, &e, [&](cudaStream_t cs) { return strassen_mul(*c, *a, *b, cutoff, accumulate ? 1 : 0, cs); }));
+    *out = new gf2_plan{g, e};
+    return GF2_OK;
+}
+
+int gf2_plan_m4rm(gf2_plan **out, const gf2_view *c, const gf2_view *a, const gf2_view *b, int k, int accumulate) {
+    if (!out) return set_error(GF2_ERR_PARAMETER, "null plan pointer");
+    *out = nullptr;
+    if (k < 1 || k > 16) return set_error(GF2_ERR_PARAMETER, "k=" + std::to_string(k) + " outside 1..16");
+    GF2_TRY(check_mul(c, a, b));
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t e = nullptr;
+    GF2_TRY(capture_plan(&g, &e, [&](cudaStream_t cs) { return base_mul(*c, *a, *b, accumulate ? 1 : 0, cs); }));
+    *out = new gf2_plan{g, e};
     return GF2_OK;
 }
 

@@ -4,6 +4,8 @@
 // running along a row so every access is a coalesced 256-byte segment.
 #include <type_traits>
 
+#include <algorithm>
+
 #include "gf2_internal.cuh"
 
 namespace gf2 {
@@ -375,11 +377,29 @@ int launch_make_table(const gf2_view &table, const gf2_view &src, int k, cudaStr
     return check_cuda(cudaGetLastError(), "k_make_table launch");
 }
 
+// narrow whole-word strips (a product target's ragged last word and
+// padding): one thread per word, grid-stride
+__global__ void k_zero_strip(u64 *data, int64_t pitch, int64_t nrows, int64_t w) {
+    pdl_begin();
+    const int64_t total = nrows * w;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+        data[(i / w) * pitch + i % w] = 0;
+}
+
 int launch_zero(const gf2_view &v, cudaStream_t s) {
     if (!v.nrows || !v.ncols) return GF2_OK;
     if (v.ncols % kWordBits) return launch_ewise(v, nullptr, nullptr, 0, s);
-    return check_cuda(cudaMemset2DAsync(v.data, (size_t)v.pitch * 8, 0, (size_t)(v.ncols / kWordBits) * 8,
-                                        (size_t)v.nrows, s),
+    const int64_t w = v.ncols / kWordBits;
+    if (w < 64 && v.nrows > 1 && v.pitch != w) {
+        // a strided 2-D memset of rows this narrow runs far below HBM speed
+        // (cfg4's 16-word strips: 6.5 us); one thread per word does not
+        const int64_t total = v.nrows * w;
+        const int64_t blocks = std::min<int64_t>((total + 255) / 256, 4 * 148);
+        GF2_LAUNCH(launch_k(k_zero_strip, dim3((unsigned)blocks), dim3(256), 0, s, 1, v.data, v.pitch, v.nrows, w));
+        note_launch();
+        return check_cuda(cudaGetLastError(), "k_zero_strip launch");
+    }
+    return check_cuda(cudaMemset2DAsync(v.data, (size_t)v.pitch * 8, 0, (size_t)w * 8, (size_t)v.nrows, s),
                       "zero");
 }
 

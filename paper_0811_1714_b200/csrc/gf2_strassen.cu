@@ -69,8 +69,12 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
     // GF2_POST_FUSE_MIN_K the leaf products are stored plainly into C_d and
     // one more combine pass folds them up (red.xor traffic, not MMA time,
     // bounds short-K tiles).
-    static const int64_t post_min_k = getenv("GF2_POST_FUSE_MIN_K") ? atoll(getenv("GF2_POST_FUSE_MIN_K")) : 0;
-    const bool fpost = L[depth] >= post_min_k;
+    // Default: 1024-deep leaves (cfg2 at the reference's cutoff 1024) store
+    // plainly -- cfg2 63.7 -> 60.6 us, 8192^3 at cutoff 1024 310 -> 285 us --
+    // while deeper leaves (2048: even; 4096+: fused faster) and the shallow
+    // 512-cutoff leaves (736 deep: fused 1.3 us faster) keep the fused form.
+    static const int64_t post_min_k = getenv("GF2_POST_FUSE_MIN_K") ? atoll(getenv("GF2_POST_FUSE_MIN_K")) : -1;
+    const bool fpost = post_min_k >= 0 ? L[depth] >= post_min_k : !(L[depth] >= 1024 && L[depth] < 2048);
     const int last = fpost ? depth - 1 : depth;  // deepest materialized C level
     // pre-addition levels fused into the expansion (GF2_FUSE_LEVELS=2 folds
     // two levels into it; one is faster on B200)

@@ -92,7 +92,12 @@ __global__ void __launch_bounds__(256) k_expand4_rows(ExpandArgs a) {
 // combinations (mask[i]) and writes each one's nibbles like k_expand4_rows
 // (output problem 7p + i). Quadrant words are read once instead of 14
 // times per 7 outputs.
-template <int ROWS>
+// LEVELS = 2 (two fused levels, block z = 7p + i): the block first forms the
+// 4 sub-quadrant words of level-0 combination i (mask[i] over the level-0
+// quadrants, up to 16 source words), then writes its 7 level-1 combinations
+// (output problem 49p + 7i + j = 7z + j) -- the level-0 operands are never
+// materialized.
+template <int ROWS, int LEVELS>
 __global__ void __launch_bounds__(256) k_expand4_rows7(ExpandArgs a) {
     pdl_begin();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -101,15 +106,31 @@ __global__ void __launch_bounds__(256) k_expand4_rows7(ExpandArgs a) {
     const int64_t r0 = ((int64_t)blockIdx.y * 8 + warp) * ROWS;
     if (r0 >= a.rows) return;
     const u64 tm = (j == width - 1) ? tail_mask(a.cols) : ~0ULL;
-    const int64_t p = a.q0 / 7 + blockIdx.z;  // source problem
+    const int64_t p = LEVELS == 1 ? a.q0 / 7 + blockIdx.z : a.q0 / 49 + blockIdx.z / 7;  // source problem
     const u64 *s = a.src + p * a.sstride + j;
     const bool live = j < width;
     u64 qw[ROWS][4];
+    if (LEVELS == 1) {
 #pragma unroll
-    for (int rr = 0; rr < ROWS; ++rr)
+        for (int rr = 0; rr < ROWS; ++rr)
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
-            qw[rr][t] = (live && r0 + rr < a.rows) ? __ldg(s + a.qoff[t] + (r0 + rr) * a.sp) & tm : 0;
+            for (int t = 0; t < 4; ++t)
+                qw[rr][t] = (live && r0 + rr < a.rows) ? __ldg(s + a.qoff[t] + (r0 + rr) * a.sp) & tm : 0;
+    } else {
+        const unsigned mi = a.mask[blockIdx.z % 7];
+#pragma unroll
+        for (int rr = 0; rr < ROWS; ++rr)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                u64 x = 0;
+                if (live && r0 + rr < a.rows) {
+#pragma unroll
+                    for (int Q = 0; Q < 4; ++Q)
+                        if (mi & (1u << Q)) x ^= __ldg(s + a.qoff[Q] + a.qoff2[t] + (r0 + rr) * a.sp);
+                }
+                qw[rr][t] = x & tm;
+            }
+    }
     const int h = lane & 1;
 #pragma unroll 1
     for (int i = 0; i < 7; ++i) {
@@ -567,7 +588,9 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
 static int launch_expand4(const ExpandArgs &a, int64_t nprob, bool cols, cudaStream_t s) {
     const int64_t width = words_per_row(a.cols);
     if (!a.rows || !width || !nprob) return GF2_OK;
-    if (!cols && a.levels == 1 && a.q0 % 7 == 0 && nprob % 7 == 0) {
+    const bool g7 = a.levels == 1 && a.q0 % 7 == 0 && nprob % 7 == 0;
+    const bool g49 = a.levels == 2 && a.q0 % 49 == 0 && nprob % 49 == 0;
+    if (!cols && (g7 || g49)) {
         // 2 rows per warp: 48 registers, more resident blocks and a finer grid
         // than 4 (43 vs 45 us at cfg3; forcing occupancy via launch bounds spills)
         // one row per warp when two would give fewer than 4 blocks per SM
@@ -575,10 +598,16 @@ static int launch_expand4(const ExpandArgs &a, int64_t nprob, bool cols, cudaStr
         const int64_t blocks2 = (width + 31) / 32 * ((a.rows + 15) / 16) * (nprob / 7);
         if (blocks2 < 4 * num_sms()) {
             dim3 grd((unsigned)((width + 31) / 32), (unsigned)((a.rows + 8 - 1) / 8), (unsigned)(nprob / 7));
-            GF2_LAUNCH(launch_k(k_expand4_rows7<1>, grd, 256, 0, s, 1, a));
+            if (g7)
+                GF2_LAUNCH(launch_k(k_expand4_rows7<1, 1>, grd, 256, 0, s, 1, a));
+            else
+                GF2_LAUNCH(launch_k(k_expand4_rows7<1, 2>, grd, 256, 0, s, 1, a));
         } else {
             dim3 grd((unsigned)((width + 31) / 32), (unsigned)((a.rows + 8 * 2 - 1) / (8 * 2)), (unsigned)(nprob / 7));
-            GF2_LAUNCH(launch_k(k_expand4_rows7<2>, grd, 256, 0, s, 1, a));
+            if (g7)
+                GF2_LAUNCH(launch_k(k_expand4_rows7<2, 1>, grd, 256, 0, s, 1, a));
+            else
+                GF2_LAUNCH(launch_k(k_expand4_rows7<2, 2>, grd, 256, 0, s, 1, a));
         }
         note_launch();
         return check_cuda(cudaGetLastError(), "k_expand4_rows7 launch");
@@ -642,6 +671,7 @@ int launch_umma_f4(const UmmaJob &jb, int64_t nprob, cudaStream_t s) {
     const int64_t cap = (int64_t)8 << 30;
     int64_t qchunk = std::max<int64_t>(1, std::min<int64_t>(nprob, cap / std::max<int64_t>(per, 1)));
     if (jb.fuse_pre == 1 && qchunk >= 7) qchunk -= qchunk % 7;  // whole 7-product groups (k_expand4_rows7)
+    if (jb.fuse_pre == 2 && qchunk >= 49) qchunk -= qchunk % 49;  // whole 49-product groups
     uint8_t *ws = nullptr;
     GF2_TRY(pool_setup());
     cudaError_t e = cudaMallocAsync((void **)&ws, (size_t)(qchunk * per), s);

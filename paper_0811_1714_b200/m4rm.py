@@ -11,9 +11,13 @@ which changes nothing in the result: the product is exact.
 Dispatch (gf2_mul_base): products past the measured crossover -- at least
 1e10 bit-ops with every side >= 640 -- run on the selected tensor engine
 (tcgen05 kind::mxf4 by default), which computes the same product faster
-(the reference's cfg4 call mul_m4rm_into(C, A, B, 8, 512, 8): 0.70 ms on the
-M4RM kernel, ~0.27 ms on tc-f4); smaller products, e.g. cfg1's 1024^3, run
+(the reference's cfg4 call mul_m4rm_into(C, A, B, 8, 512, 8): 0.54 ms on the
+M4RM kernel, ~0.28 ms on tc-f4); smaller products, e.g. cfg1's 1024^3, run
 the M4RM kernel. set_engine("m4rm") forces the M4RM kernel everywhere.
+
+M4rmPlan captures one such product on fixed matrices as a CUDA graph
+(gf2_plan_m4rm): for small products the host path (validation, geometry,
+tensor maps, up to three launches) costs more than the kernel.
 """
 
 from __future__ import annotations
@@ -93,3 +97,38 @@ def mul_m4rm_into(c: BitMatrix, a: Mat, b: Mat, k: int,
         raise DimensionError(
             f"target {c.nrows}x{c.ncols} != product {a.nrows}x{b.ncols}")
     _mul_into(c, a, b, k, True)
+
+
+class M4rmPlan:
+    """A captured mul_m4rm / mul_m4rm_into (CUDA graph, gf2_plan_m4rm):
+    C = A.B (or C ^= A.B with accumulate=True) on these matrices, replayed
+    by `run()` with one graph launch. Each run reads the operands' current
+    contents; the plan keeps its matrices alive."""
+
+    def __init__(self, c: Mat, a: Mat, b: Mat, k: int = 8, accumulate: bool = False):
+        import ctypes
+        _validate(a, b, k, 1, 1)
+        if c.nrows != a.nrows or c.ncols != b.ncols:
+            raise DimensionError(
+                f"target {c.nrows}x{c.ncols} != product {a.nrows}x{b.ncols}")
+        _check_cuda_dev(c, a, b)
+        self._mats = (c, a, b)
+        self._lib = _lib.lib_cuda()
+        h = ctypes.c_void_p()
+        _lib.check(self._lib.gf2_plan_m4rm(ctypes.byref(h), c._view(), a._view(), b._view(),
+                                           int(k), int(accumulate)))
+        self._h = h
+
+    @property
+    def c(self):
+        return self._mats[0]
+
+    def run(self) -> None:
+        """Launch the captured product on the current stream."""
+        _lib.check(self._lib.gf2_plan_launch(self._h, _stream()))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.gf2_plan_destroy(h)
+            self._h = None

@@ -234,12 +234,14 @@ def test_two_fused_levels_option(engine, digests):
 
 
 @pytest.mark.parametrize("engine", ["tc-f4", "tc-i8"])
-def test_unfused_post_additions(engine, digests):
-    """GF2_POST_FUSE_MIN_K above the leaf depth (read once per process,
-    hence a subprocess): the leaf products are stored plainly into their own
-    level and one more combine pass folds them up, instead of the GEMM
-    epilogue XORing each product into its destination quadrants. cfg2 at the
-    reference's cutoff (depth 2) and an accumulate into a window."""
+@pytest.mark.parametrize("min_k", ["1000000", "0"])
+def test_unfused_post_additions(engine, min_k, digests):
+    """GF2_POST_FUSE_MIN_K (read once per process, hence a subprocess) above
+    the leaf depth: the leaf products are stored plainly into their own
+    level and one more combine pass folds them up (the default for
+    1024-deep leaves); 0: the GEMM epilogue XORs each product into its
+    destination quadrants (the default elsewhere). cfg2 at the reference's
+    cutoff (depth 2) and an accumulate into a window."""
     import os
     import subprocess
     import sys
@@ -261,7 +263,7 @@ def test_unfused_post_additions(engine, digests):
         "exp = before.copy(); exp[7:7 + 4096, 1:1 + 64] ^= ref\n"
         "print(bool((after == exp).all()))\n"
     ) % (root, engine)
-    env = dict(os.environ, GF2_POST_FUSE_MIN_K="1000000")
+    env = dict(os.environ, GF2_POST_FUSE_MIN_K=min_k)
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root,
                          capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
@@ -411,4 +413,36 @@ def test_strassen_plan_graph_replay(engine, digests):
     p2.run()
     p2.run()                                    # C + AB + AB = C
     assert np.array_equal(words(acc), acc0)
+    del plan, p2
+
+
+@pytest.mark.parametrize("shape", [(1024, 1024, 1024), (200, 300, 130), (2048, 2048, 4096)])
+def test_m4rm_plan_graph_replay(shape, digests):
+    """M4rmPlan (CUDA graph of one mul_m4rm / mul_m4rm_into): replays equal
+    the eager product (cfg1's digest at 1024^3; the 2048x2048x4096 product
+    is past the crossover, so the graph holds the tensor-core path), read
+    the operands' current contents, and accumulate (C + AB + AB = C)."""
+    import torch
+    m, l, n = shape
+    seed = 11 if shape == (1024, 1024, 1024) else 3
+    a, b = g.random(m, l, seed), g.random(l, n, seed + 1)
+    c = g.create(m, n)
+    plan = g.M4rmPlan(c, a, b, 8)
+    for _ in range(3):
+        plan.run()
+    torch.cuda.synchronize()
+    if shape == (1024, 1024, 1024):
+        assert O.digest(words(c)) == digests["cfg1"]
+    assert g.equal(c, g.mul_m4rm(a, b, 8))
+    g.copy_into(a, g.random(m, l, 99))
+    plan.run()
+    assert g.equal(c, g.mul_m4rm(a, b, 8))
+    acc = g.random(m, n, 5)
+    acc0 = words(acc)
+    p2 = g.M4rmPlan(acc, a, b, 8, accumulate=True)
+    p2.run()
+    p2.run()
+    assert np.array_equal(words(acc), acc0)
+    with pytest.raises(g.DimensionError):
+        g.M4rmPlan(g.create(m + 1, n), a, b, 8)
     del plan, p2

@@ -42,6 +42,7 @@ def med(fn, reps=200):
     return ts[len(ts) // 2] * 1e6
 
 
+plan1 = g.M4rmPlan(c, a, b, 8)
 rows = [
     ("torch.empty(1024x16 i64)", lambda: torch.empty((1024, 16), dtype=torch.int64, device=dev)),
     ("torch.zeros(1024x16 i64)", lambda: torch.zeros((1024, 16), dtype=torch.int64, device=dev)),
@@ -55,6 +56,7 @@ rows = [
     ("lib.gf2_add (one ewise launch)", lambda: lib.gf2_add(vc, va, vb, s)),
     ("lib.gf2_m4rm accumulate (1 launch + maps)", lambda: lib.gf2_m4rm(vc, va, vb, 8, 1, s)),
     ("g.mul_m4rm(a,b,8)", lambda: g.mul_m4rm(a, b, 8)),
+    ("M4rmPlan(c,a,b,8).run()", plan1.run),
     ("lib.gf2_strassen 4096 cutoff 1024", lambda: lib.gf2_strassen(c2._view(), a2._view(), b2._view(), 1024, 8, 0, s)),
     ("g.mul_strassen 4096 cutoff 1024", lambda: g.mul_strassen(a2, b2, p2)),
     ("g.mul_strassen 4096 default", lambda: g.mul_strassen(a2, b2)),

@@ -73,10 +73,16 @@ def main():
     cases = []
     a1, b1 = g.random(1024, 1024, 11), g.random(1024, 1024, 12)
     cases.append(("cfg1 mul_m4rm(A,B,8) 1024^3", lambda: g.mul_m4rm(a1, b1, 8)))
+    c1 = g.create(1024, 1024)
+    plan1 = g.M4rmPlan(c1, a1, b1, 8)
+    cases.append(("cfg1 M4rmPlan.run() 1024^3", plan1.run))
     a2, b2 = g.random(4096, 4096, 21), g.random(4096, 4096, 22)
     p2 = g.MulParams(cutoff=1024, k=8)
     cases.append(("cfg2 mul_strassen cutoff 1024", lambda: g.mul_strassen(a2, b2, p2)))
     cases.append(("cfg2 mul_strassen default", lambda: g.mul_strassen(a2, b2)))
+    c2 = g.create(4096, 4096)
+    plan2 = g.StrassenPlan(c2, a2, b2, p2)
+    cases.append(("cfg2 StrassenPlan.run() cutoff 1024", plan2.run))
     a4 = g.bernoulli(10000, 7001, 41, 0.1)
     b4 = g.bernoulli(7001, 12345, 42, 0.1)
     c4 = g.random(10000, 12345, 43)
