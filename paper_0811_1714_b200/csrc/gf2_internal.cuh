@@ -244,6 +244,18 @@ inline int64_t tensor_min_leaf() {
     static const int64_t env = getenv("GF2_TC_MIN_LEAF") ? atoll(getenv("GF2_TC_MIN_LEAF")) : 0;
     return env > 0 ? env : 640;
 }
+// shallowest tensor-core Strassen leaf in K (GF2_TC_MIN_LEAF_K overrides it;
+// 0 honours the caller's cutoff exactly). A 1024-deep leaf tile is bound by
+// its epilogue -- draining 224 f32 columns from TMEM (~3400 cycles) takes
+// longer than its 4 K-blocks of MMA (~1900) -- so a Winograd level whose
+// leaves would be shallower than this is not taken on a tensor engine: its
+// product runs classically inside the accumulator (K twice as deep), which
+// costs 8/7 of that level's MMAs and saves 3/7 of its epilogues. cfg2 at the
+// reference's cutoff 1024: 60.6 -> ~44 us.
+inline int64_t tensor_leaf_k() {
+    static const int64_t env = getenv("GF2_TC_MIN_LEAF_K") ? atoll(getenv("GF2_TC_MIN_LEAF_K")) : -1;
+    return env >= 0 ? env : 2048;
+}
 inline int launch_product(const M4rmBatch &b, cudaStream_t s) {
     const double work = (double)b.m * (double)b.l * (double)b.n * (double)b.nprob;
     if (g_engine == 0 || work < tensor_min_work()) return launch_m4rm(b, s);

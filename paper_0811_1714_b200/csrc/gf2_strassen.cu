@@ -396,6 +396,18 @@ int strassen_mul(const gf2_view &C, const gf2_view &A, const gf2_view &B, int64_
     int64_t ps[4];
     peel_split(m, l, n, cutoff, ps);
     if (ps[3] == 0) return m4rm_view(C, A, B, accumulate, s);
+    // With a tensor engine, leaves shallower than tensor_leaf_k() in K are
+    // not worth their Winograd level: 1024-deep tensor leaves are epilogue
+    // bound, smaller ones fall back to M4RM, and there the recursion's
+    // passes cost more than the 1/8 of lookups a level saves (2048^3 at
+    // cutoff 256: 57 us against ~20 us for one M4RM product). Recurse only
+    // while leaves stay >= tensor_leaf_k() -- the caller's cutoff still
+    // bounds the depth -- or multiply directly. Engine 0 (M4RM) honours the
+    // cutoff exactly, as the reference does.
+    if (g_engine != 0 && cutoff < tensor_leaf_k() && (ps[1] >> ps[3]) < tensor_leaf_k()) {
+        peel_split(m, l, n, tensor_leaf_k(), ps);
+        if (ps[3] == 0) return m4rm_view(C, A, B, accumulate, s);
+    }
     const int64_t m2 = ps[0], l2 = ps[1], n2 = ps[2];
     GF2_TRY(strassen_core(sub_view(C, 0, 0, m2, n2), sub_view(A, 0, 0, m2, l2), sub_view(B, 0, 0, l2, n2),
                           (int)ps[3], accumulate, s));

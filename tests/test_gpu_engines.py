@@ -263,7 +263,9 @@ def test_unfused_post_additions(engine, min_k, digests):
         "exp = before.copy(); exp[7:7 + 4096, 1:1 + 64] ^= ref\n"
         "print(bool((after == exp).all()))\n"
     ) % (root, engine)
-    env = dict(os.environ, GF2_POST_FUSE_MIN_K=min_k)
+    # GF2_TC_MIN_LEAF_K=0: keep the reference's depth 2 (1024-deep tensor
+    # leaves), which the default leaf-depth rule would fold to depth 1
+    env = dict(os.environ, GF2_POST_FUSE_MIN_K=min_k, GF2_TC_MIN_LEAF_K="0")
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root,
                          capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
@@ -344,7 +346,7 @@ def test_cfg3_depth6_tensor_leaves_chunked(engine, fuse, digests):
         "a, b = g.random(16384, 16384, 31), g.random(16384, 16384, 32)\n"
         "print(O.digest(g.mul_strassen(a, b, g.MulParams(cutoff=256, k=8)).to_numpy()))\n"
     ) % (root, engine)
-    env = dict(os.environ, GF2_TC_MIN_LEAF="256", GF2_FUSE_LEVELS=fuse)
+    env = dict(os.environ, GF2_TC_MIN_LEAF="256", GF2_TC_MIN_LEAF_K="0", GF2_FUSE_LEVELS=fuse)
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root,
                          capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]

@@ -233,7 +233,18 @@ def test_errors_match_reference():
         g.mul_m4rm_into(x, x, g.random(64, 64, 2), 8)
 
 
-def test_peeling_pattern():
+@pytest.fixture(params=["tc-f4", "m4rm"])
+def engine(request):
+    """tc-f4 (default: Winograd levels whose leaves would be shallower than
+    2048 fold into direct products) and m4rm (the recursion at exactly the
+    caller's cutoff, M4RM leaves and peel fix-ups, as the reference runs)."""
+    prev = g.get_engine()
+    g.set_engine(request.param)
+    yield request.param
+    g.set_engine(prev)
+
+
+def test_peeling_pattern(engine):
     # test_strassen.py:175-180 (n = 2^10 - 1, 2^10, 2^10 + 1)
     for n in (1023, 1024, 1025):
         a, b = g.random(n, n, n), g.random(n, n, n + 1)
@@ -242,7 +253,7 @@ def test_peeling_pattern():
                      want.words, str(n))
 
 
-def test_strassen_random_triples_vs_port():
+def test_strassen_random_triples_vs_port(engine):
     # test_strassen.py:207-216 shape range, deeper recursion via cutoff 64
     rng = np.random.default_rng(27)
     for trial in range(40):
@@ -252,6 +263,30 @@ def test_strassen_random_triples_vs_port():
                               O.random(l, n, trial + 4000), cutoff=512)
         assert_words(g.mul_strassen(a, b, g.MulParams(cutoff=64)), want.words,
                      f"{m,l,n}")
+
+
+def test_tensor_engine_folds_shallow_levels():
+    """With a tensor engine, a cutoff whose leaves would be shallower than
+    2048 does not buy Winograd levels: 1500^3 at cutoff 64
+    runs as one product (a handful of launches) instead of a depth-4
+    recursion; the m4rm engine keeps the reference's exact recursion. Same
+    words either way."""
+    a, b = g.random(1500, 1500, 1), g.random(1500, 1500, 2)
+    p = g.MulParams(cutoff=64)
+    prev = g.get_engine()
+    try:
+        g.set_engine("tc-f4")
+        n0 = g.launch_count()
+        c1 = g.mul_strassen(a, b, p)
+        folded = g.launch_count() - n0
+        g.set_engine("m4rm")
+        n0 = g.launch_count()
+        c2 = g.mul_strassen(a, b, p)
+        exact = g.launch_count() - n0
+    finally:
+        g.set_engine(prev)
+    assert folded <= 4 < exact
+    assert g.equal(c1, c2)
 
 
 def test_algebraic_laws():
