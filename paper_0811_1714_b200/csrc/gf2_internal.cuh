@@ -264,6 +264,9 @@ inline int launch_product(const M4rmBatch &b, cudaStream_t s) {
 // cuTensorMapEncodeTiled through the runtime's driver entry point: a 3-D
 // map (inner, outer, problems), byte strides for dims 1 and 2, no
 // interleave, 128-byte swizzle or none, OOB elements read as zero.
+// rank 1..5 (dims[0] innermost; strides[i] = bytes between steps of dim i+1)
+int encode_map_nd(CUtensorMap *map, CUtensorMapDataType dt, void *base, int rank, const uint64_t *dims,
+                  const uint64_t *strides, const uint32_t *box, bool swizzle128);
 int encode_map_3d(CUtensorMap *map, CUtensorMapDataType dt, void *base, const uint64_t dims[3],
                   const uint64_t strides[2], const uint32_t box[3], bool swizzle128);
 int timer_enable(int on);

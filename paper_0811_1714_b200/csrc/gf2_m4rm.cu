@@ -363,6 +363,310 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+
+// ------------------------------------------------------------------ BM = 8192
+// Taller tile, same shared-memory budget: 16 rows per thread, 8 of them in
+// registers and 8 parked in tensor memory (TMEM, 512 columns per CTA). Per
+// A half-word a thread looks its register rows up, swaps them with the
+// parked ones (tcgen05.st + tcgen05.ld: TMEM's own datapath, not the
+// shared-memory port the lookups saturate) and looks those up. Every table
+// then serves 8192 rows: the build costs 256/8192 of the lookup traffic.
+// Stages are one A half-word (32 KiB of the half-word-major A^T, one 5-D TMA
+// box) in a 3-slot ring, B half panels (1 KiB) in an 8-slot ring, and the
+// 3-slot half-word table ring of k_m4rm.
+constexpr int kTmRows = 8192;
+constexpr int kTmA = kTmRows * 4;   // one A half-word for 8192 rows
+constexpr int kTmNA = 3;
+constexpr int kTmNB = 8;
+constexpr int kTmB = 32 * 32;       // 32 rows x 32 B
+constexpr int kTmSmem = kNT * kTabBytes + kTmNA * kTmA + kTmNB * kTmB + 256;
+
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void lds128v(uint32_t addr, uint32_t &a, uint32_t &b, uint32_t &c, uint32_t &d) {
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(addr));
+}
+__device__ __forceinline__ void tma_5d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, int c3, int c4,
+                                       uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+        "%6}], [%7];\n" ::"r"(dst),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
+        : "memory");
+}
+// 8 rows x 8 words of accumulators <-> 64 TMEM columns of this thread's lane
+__device__ __forceinline__ void tm_store(uint32_t taddr, const uint32_t (&x)[8][8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63, %64};\n" ::"r"(taddr), "r"(x[0][0]), "r"(x[0][1]), "r"(x[0][2]), "r"(x[0][3]), "r"(x[0][4]), "r"(x[0][5]), "r"(x[0][6]), "r"(x[0][7]), "r"(x[1][0]), "r"(x[1][1]), "r"(x[1][2]), "r"(x[1][3]), "r"(x[1][4]), "r"(x[1][5]), "r"(x[1][6]), "r"(x[1][7]), "r"(x[2][0]), "r"(x[2][1]), "r"(x[2][2]), "r"(x[2][3]), "r"(x[2][4]), "r"(x[2][5]), "r"(x[2][6]), "r"(x[2][7]), "r"(x[3][0]), "r"(x[3][1]), "r"(x[3][2]), "r"(x[3][3]), "r"(x[3][4]), "r"(x[3][5]), "r"(x[3][6]), "r"(x[3][7]), "r"(x[4][0]), "r"(x[4][1]), "r"(x[4][2]), "r"(x[4][3]), "r"(x[4][4]), "r"(x[4][5]), "r"(x[4][6]), "r"(x[4][7]), "r"(x[5][0]), "r"(x[5][1]), "r"(x[5][2]), "r"(x[5][3]), "r"(x[5][4]), "r"(x[5][5]), "r"(x[5][6]), "r"(x[5][7]), "r"(x[6][0]), "r"(x[6][1]), "r"(x[6][2]), "r"(x[6][3]), "r"(x[6][4]), "r"(x[6][5]), "r"(x[6][6]), "r"(x[6][7]), "r"(x[7][0]), "r"(x[7][1]), "r"(x[7][2]), "r"(x[7][3]), "r"(x[7][4]), "r"(x[7][5]), "r"(x[7][6]), "r"(x[7][7]) : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tm_load(uint32_t taddr, uint32_t (&x)[8][8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63}, [%64];\n" : "=r"(x[0][0]), "=r"(x[0][1]), "=r"(x[0][2]), "=r"(x[0][3]), "=r"(x[0][4]), "=r"(x[0][5]), "=r"(x[0][6]), "=r"(x[0][7]), "=r"(x[1][0]), "=r"(x[1][1]), "=r"(x[1][2]), "=r"(x[1][3]), "=r"(x[1][4]), "=r"(x[1][5]), "=r"(x[1][6]), "=r"(x[1][7]), "=r"(x[2][0]), "=r"(x[2][1]), "=r"(x[2][2]), "=r"(x[2][3]), "=r"(x[2][4]), "=r"(x[2][5]), "=r"(x[2][6]), "=r"(x[2][7]), "=r"(x[3][0]), "=r"(x[3][1]), "=r"(x[3][2]), "=r"(x[3][3]), "=r"(x[3][4]), "=r"(x[3][5]), "=r"(x[3][6]), "=r"(x[3][7]), "=r"(x[4][0]), "=r"(x[4][1]), "=r"(x[4][2]), "=r"(x[4][3]), "=r"(x[4][4]), "=r"(x[4][5]), "=r"(x[4][6]), "=r"(x[4][7]), "=r"(x[5][0]), "=r"(x[5][1]), "=r"(x[5][2]), "=r"(x[5][3]), "=r"(x[5][4]), "=r"(x[5][5]), "=r"(x[5][6]), "=r"(x[5][7]), "=r"(x[6][0]), "=r"(x[6][1]), "=r"(x[6][2]), "=r"(x[6][3]), "=r"(x[6][4]), "=r"(x[6][5]), "=r"(x[6][6]), "=r"(x[6][7]), "=r"(x[7][0]), "=r"(x[7][1]), "=r"(x[7][2]), "=r"(x[7][3]), "=r"(x[7][4]), "=r"(x[7][5]), "=r"(x[7][6]), "=r"(x[7][7]) : "r"(taddr) : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+// store the register group to one TMEM slot and load the other into the
+// same registers, in one asm statement: the accumulators keep their
+// registers across the swap (as two statements the compiler gave the
+// loaded group a second register set and spilled)
+__device__ __forceinline__ void tm_swap(uint32_t st_addr, uint32_t ld_addr, uint32_t (&x)[8][8]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x64.b32 [%64], {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63};\n"
+        "tcgen05.wait::st.sync.aligned;\n"
+        "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63}, [%65];\n"
+        "tcgen05.wait::ld.sync.aligned;\n"
+        : "+r"(x[0][0]), "+r"(x[0][1]), "+r"(x[0][2]), "+r"(x[0][3]), "+r"(x[0][4]), "+r"(x[0][5]), "+r"(x[0][6]), "+r"(x[0][7]), "+r"(x[1][0]), "+r"(x[1][1]), "+r"(x[1][2]), "+r"(x[1][3]), "+r"(x[1][4]), "+r"(x[1][5]), "+r"(x[1][6]), "+r"(x[1][7]), "+r"(x[2][0]), "+r"(x[2][1]), "+r"(x[2][2]), "+r"(x[2][3]), "+r"(x[2][4]), "+r"(x[2][5]), "+r"(x[2][6]), "+r"(x[2][7]), "+r"(x[3][0]), "+r"(x[3][1]), "+r"(x[3][2]), "+r"(x[3][3]), "+r"(x[3][4]), "+r"(x[3][5]), "+r"(x[3][6]), "+r"(x[3][7]), "+r"(x[4][0]), "+r"(x[4][1]), "+r"(x[4][2]), "+r"(x[4][3]), "+r"(x[4][4]), "+r"(x[4][5]), "+r"(x[4][6]), "+r"(x[4][7]), "+r"(x[5][0]), "+r"(x[5][1]), "+r"(x[5][2]), "+r"(x[5][3]), "+r"(x[5][4]), "+r"(x[5][5]), "+r"(x[5][6]), "+r"(x[5][7]), "+r"(x[6][0]), "+r"(x[6][1]), "+r"(x[6][2]), "+r"(x[6][3]), "+r"(x[6][4]), "+r"(x[6][5]), "+r"(x[6][6]), "+r"(x[6][7]), "+r"(x[7][0]), "+r"(x[7][1]), "+r"(x[7][2]), "+r"(x[7][3]), "+r"(x[7][4]), "+r"(x[7][5]), "+r"(x[7][6]), "+r"(x[7][7])
+        : "r"(st_addr), "r"(ld_addr)
+        : "memory");
+}
+
+// A^T half-word-major: At[p][w][h][r] (u32; h = 0 the high half = K rows
+// 0..31 of word w), l-tail masked, rows padded to mp (a multiple of 256)
+// with zeros.
+__global__ void __launch_bounds__(256) k_words_th(const u64 *A, int64_t pa, int64_t sa, uint32_t *At, int64_t mp,
+                                                  int64_t m, int64_t Wl, u64 atm) {
+    pdl_begin();
+    __shared__ u64 t[32][33];
+    const int64_t prob = blockIdx.z;
+    const int64_t r0 = (int64_t)blockIdx.x * 32, w0 = (int64_t)blockIdx.y * 32;
+    const u64 *a = A + prob * sa;
+    uint32_t *o = At + prob * Wl * 2 * mp;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = ty; j < 32; j += 8) {
+        const int64_t r = r0 + j, w = w0 + tx;
+        u64 v = 0;
+        if (r < m && w < Wl) {
+            v = a[r * pa + w];
+            if (w == Wl - 1) v &= atm;
+        }
+        t[j][tx] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = ty; j < 32; j += 8) {
+        const int64_t w = w0 + j, r = r0 + tx;
+        if (w < Wl && r < mp) {
+            const u64 v = t[tx][j];
+            o[(w * 2 + 0) * mp + r] = (uint32_t)(v >> 32);
+            o[(w * 2 + 1) * mp + r] = (uint32_t)v;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_m4rm_tm(KArgs p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const uint32_t s_tab = (uint32_t)__cvta_generic_to_shared(smem);
+    const uint32_t s_a = s_tab + kNT * kTabBytes;
+    const uint32_t s_b = s_a + kTmNA * kTmA;
+    const uint32_t s_bar = s_b + kTmNB * kTmB;
+    const uint32_t b_tfull = s_bar, b_tempty = s_bar + 24, b_afull = s_bar + 48, b_aempty = s_bar + 72,
+                   b_bfull = s_bar + 96;  // 8 barriers
+    const uint32_t s_tmem = s_bar + 160;
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+
+    // 32-bit coordinates (TMA coordinates are 32-bit anyway): fewer live
+    // registers beside the 64 accumulator words
+    const int prob = (int)(blockIdx.z / p.nsplit);
+    const int split = (int)(blockIdx.z % p.nsplit);
+    const int col_w0 = (int)blockIdx.x * kTileWords;
+    const int rb0 = (int)blockIdx.y * (kTmRows / 256);  // first 256-row block
+    const int kw0 = split * (int)p.kws;
+    const int kw1 = (int)min((int64_t)kw0 + p.kws, p.Wl);
+    const int nwords = kw1 > kw0 ? kw1 - kw0 : 0;
+    const int H = 2 * nwords;
+
+    if (tid == 0) {
+        for (int i = 0; i < 3; ++i) {
+            mbar_init(b_tfull + 8 * i, 2);
+            mbar_init(b_tempty + 8 * i, kThreads / 32);
+            mbar_init(b_afull + 8 * i, 1);
+            mbar_init(b_aempty + 8 * i, kThreads / 32);
+        }
+        for (int i = 0; i < kTmNB; ++i) mbar_init(b_bfull + 8 * i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(s_tmem) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tbase = *reinterpret_cast<volatile uint32_t *>(smem + (s_tmem - s_tab));
+    pdl_begin();
+
+    auto issue_a = [&](int h) {
+        const uint32_t bar = b_afull + 8 * (h % kTmNA);
+        mbar_expect(bar, kTmA);
+        tma_5d(s_a + (h % kTmNA) * kTmA, &tmA, 0, rb0, h & 1, kw0 + (h >> 1), prob, bar);
+    };
+    auto issue_b = [&](int h) {
+        const uint32_t bar = b_bfull + 8 * (h % kTmNB);
+        mbar_expect(bar, kTmB);
+        tma_3d(s_b + (h % kTmNB) * kTmB, &tmB, col_w0, kw0 * 64 + 32 * h, prob, bar);
+    };
+    if (tid == 0) {
+        for (int h = 0; h < H && h < kTmNA; ++h) issue_a(h);
+        for (int h = 0; h < H && h < kTmNB; ++h) issue_b(h);
+    }
+
+    // builder role (pair h & 7 builds half-word h)
+    const int bt = tid & 63;
+    const int tj = (bt >> 1) & 3;
+    const int bs = bt & 1;
+    const int sg = bt >> 3;
+    auto build = [&](int h) {
+        const int slot = h % kNT;
+        const u64 bm0 = col_mask(col_w0 + 2 * bs, p.Wn, tail_mask(p.n));
+        const u64 bm1 = col_mask(col_w0 + 2 * bs + 1, p.Wn, tail_mask(p.n));
+        if (h >= kNT) mbar_wait(b_tempty + 8 * slot, ((h - kNT) / kNT) & 1);
+        mbar_wait(b_bfull + 8 * (h % kTmNB), (h / kTmNB) & 1);
+        const uint32_t rb = s_b + (h % kTmNB) * kTmB + (8 * tj) * 32 + bs * 16;
+        u64 c0 = 0, c1 = 0;
+        u64 x0[5], x1[5];
+#pragma unroll
+        for (int e = 0; e < 5; ++e) x0[e] = x1[e] = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int j = (i + tj) & 7;  // rows of the 4 tables in 4 bank quarters
+            u64 y0, y1;
+            lds128(rb + j * 32, y0, y1);
+            y0 &= bm0;
+            y1 &= bm1;
+            const bool hi = (j < 3) && ((sg >> (2 - j)) & 1);
+            c0 ^= hi ? y0 : 0ULL;
+            c1 ^= hi ? y1 : 0ULL;
+#pragma unroll
+            for (int e = 0; e < 5; ++e) {
+                x0[e] = (j == 3 + e) ? y0 : x0[e];
+                x1[e] = (j == 3 + e) ? y1 : x1[e];
+            }
+        }
+        const uint32_t ts = s_tab + slot * kTabBytes + (sg * 32) * 128 + tj * 32 + bs * 16;
+        sts128(ts, c0, c1);
+#pragma unroll
+        for (int i = 1; i < 32; ++i) {
+            const int b = (i & 1) ? 0 : (i & 2) ? 1 : (i & 4) ? 2 : (i & 8) ? 3 : 4;
+            const int g = i ^ (i >> 1);
+            c0 ^= x0[4 - b];
+            c1 ^= x1[4 - b];
+            sts128(ts + g * 128, c0, c1);
+        }
+        warp_arrive(b_tfull + 8 * slot, lane);
+    };
+
+    const int q = (lane >> 1) & 3;
+    const int par = lane & 1;
+
+    // accumulators of the register group: row i, u32 words 0..3 = slice par,
+    // 4..7 = slice 1-par; the other group parked at TMEM columns slot*64
+    uint32_t acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[i][e] = 0;
+    const uint32_t tlane = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 128);
+    tm_store(tlane + 64, acc);  // group 1 starts at zero
+    int cur = 0;
+
+    const int pair = warp >> 1;
+    if (pair == 0 && H > 0) build(0);
+    if (pair == 1 && H > 1) build(1);
+
+    auto lookups = [&](uint32_t tb, const uint32_t (&a)[8]) {
+        const uint32_t tq = s_tab + tb + (par << 4);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t hw = a[i];
+            const uint32_t r = __funnelshift_l(hw, hw, 8 * q);  // byte 3-t <-> table (q+t)&3
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {  // one lookup (two 16-byte slices) at a time: fewer live registers
+                const uint32_t ad = tq + (((q + t) & 3) << 5) + (((r >> (24 - 8 * t)) & 0xFF) << 7);
+                uint32_t v[8];
+                lds128v(ad, v[0], v[1], v[2], v[3]);
+                lds128v(ad ^ 16, v[4], v[5], v[6], v[7]);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[i][e] ^= v[e];
+            }
+        }
+    };
+
+    uint32_t a[8];
+    for (int h = 0; h < H; ++h) {
+        const int slot = h % kNT;
+        const uint32_t sa = s_a + (h % kTmNA) * kTmA + tid * 4;
+        mbar_wait(b_tfull + 8 * slot, (h / kNT) & 1);
+        mbar_wait(b_afull + 8 * (h % kTmNA), (h / kTmNA) & 1);
+        const uint32_t tb = slot * kTabBytes;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = lds32(sa + (cur * 4096 + i * kThreads) * 4);
+        lookups(tb, a);
+        tm_swap(tlane + cur * 64, tlane + (cur ^ 1) * 64, acc);
+        cur ^= 1;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = lds32(sa + (cur * 4096 + i * kThreads) * 4);
+        warp_arrive(b_aempty + 8 * (h % kTmNA), lane);
+        lookups(tb, a);
+        warp_arrive(b_tempty + 8 * slot, lane);
+        if (tid == 0) {
+            // A slot of half-word h-1 takes h+2 once every warp has read it;
+            // B slot of h-2 (built two iterations ago: tfull(h-2) seen) takes h+6
+            if (h >= 1 && h + 2 < H) {
+                mbar_wait(b_aempty + 8 * ((h - 1) % kTmNA), ((h - 1) / kTmNA) & 1);
+                issue_a(h + 2);
+            }
+            if (h >= 2 && h + 6 < H) issue_b(h + 6);
+        }
+        if (h + 2 < H && pair == ((h + 2) & 7)) build(h + 2);
+    }
+
+    // ---- epilogue: both groups (the register one, then the parked one)
+    u64 *C = p.C + (int64_t)prob * p.sc;
+    const u64 ntm = tail_mask(p.n);
+    const int64_t row0 = (int64_t)rb0 * 256;
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+        if (pass) {
+            cur ^= 1;
+            tm_load(tlane + cur * 64, acc);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int64_t row = row0 + cur * 4096 + i * kThreads + tid;
+            if (row >= p.m) continue;
+            u64 *crow = C + row * p.pc;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int64_t wi = col_w0 + ((e < 2) ? 2 * par : 2 * (1 - par)) + (e & 1);
+                if (wi >= p.Wn) continue;
+                const u64 v = (u64)acc[i][2 * e] | ((u64)acc[i][2 * e + 1] << 32);
+                if (p.mode == 2) {
+                    if (v) atomicXor(reinterpret_cast<unsigned long long *>(crow + wi), (unsigned long long)v);
+                } else if (p.mode == 1) {
+                    crow[wi] ^= v;
+                } else if (wi == p.Wn - 1 && ntm != ~0ULL) {
+                    crow[wi] = (crow[wi] & ~ntm) | v;
+                } else {
+                    crow[wi] = v;
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase) : "memory");
+    }
+}
+
 template <int RPT, bool DIRECT>
 int launch_rpt(const KArgs &ka, const CUtensorMap &ta, const CUtensorMap &tb, int64_t col_tiles, int64_t row_tiles,
                int64_t zdim, cudaStream_t s) {
@@ -485,7 +789,7 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     int64_t kws = Wl;
     {
         double best = 0;
-        for (int r : {8, 4, 2, 1}) {
+        for (int r : {16, 8, 4, 2, 1}) {
             const int64_t rt = (b.m + kThreads * r - 1) / (kThreads * r);
             const int64_t tiles = rt * col_tiles * b.nprob;
             for (int64_t n = 1; n <= 16 && n <= Wl; ++n) {
@@ -509,7 +813,7 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
         // tuning override, GF2_M4RM_GEOM="rpt,nsplit" (tools/ only)
         static const char *geom = getenv("GF2_M4RM_GEOM");
         int r = 0, n = 0;
-        if (geom && sscanf(geom, "%d,%d", &r, &n) == 2 && (r == 1 || r == 2 || r == 4 || r == 8) && n >= 1 &&
+        if (geom && sscanf(geom, "%d,%d", &r, &n) == 2 && (r == 1 || r == 2 || r == 4 || r == 8 || r == 16) && n >= 1 &&
             n <= 16) {
             rpt = r;
             kws = (Wl + n - 1) / n;
@@ -529,7 +833,8 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     GF2_TRY(pool_setup());
     const bool direct = rpt <= 4 && (uintptr_t)b.A % 16 == 0 && b.pa % 2 == 0 && (b.nprob == 1 || b.sa % 2 == 0) &&
                         b.m * Wl * b.nprob <= (int64_t(1) << 20);
-    const int64_t mp = (b.m + 1) & ~int64_t(1);
+    const bool tm = rpt == 16;  // BM 8192, TMEM-parked rows, half-word-major A^T
+    const int64_t mp = tm ? (b.m + 255) & ~int64_t(255) : (b.m + 1) & ~int64_t(1);
     const bool b_ok = ((uintptr_t)b.B % 16 == 0) && (b.pb % 2 == 0) && (b.nprob == 1 || b.sb % 2 == 0);
     const int64_t wnp = (Wn + 1) & ~int64_t(1);
     const int64_t at_words = direct ? 0 : b.nprob * Wl * mp;
@@ -543,7 +848,13 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     const u64 *Bm = b.B;
     int64_t pb = b.pb, sb = b.sb;
     int rc = GF2_OK;
-    if (!direct) {
+    if (tm) {
+        dim3 grid((unsigned)(mp / 32), (unsigned)((Wl + 31) / 32), (unsigned)b.nprob);
+        cudaError_t le = launch_k(k_words_th, grid, dim3(256), 0, s, 1, b.A, b.pa, b.sa, (uint32_t *)At, mp, b.m,
+                                  Wl, tail_mask(b.l));
+        if (le != cudaSuccess) rc = check_cuda(le, "k_words_th launch");
+        else note_launch();
+    } else if (!direct) {
         dim3 grid((unsigned)((b.m + 31) / 32), (unsigned)((Wl + 31) / 32), (unsigned)b.nprob);
         cudaError_t le = launch_k(k_words_t, grid, dim3(256), 0, s, 1, b.A, b.pa, b.sa, At, mp, b.m, Wl,
                                   tail_mask(b.l));
@@ -562,7 +873,17 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
         sb = b.l * wnp;
     }
     CUtensorMap ta{}, tb{};
-    if (rc == GF2_OK) {
+    if (rc == GF2_OK && tm) {
+        // A^T half-word-major (u32): 256 rows x row blocks x halves x words x problems
+        const uint64_t da[5] = {256, (uint64_t)(mp / 256), 2, (uint64_t)Wl, (uint64_t)b.nprob};
+        const uint64_t sa[4] = {1024, (uint64_t)mp * 4, (uint64_t)mp * 8, (uint64_t)(Wl * mp) * 8};
+        const uint32_t ba[5] = {256, kTmRows / 256, 1, 1, 1};
+        rc = encode_map_nd(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT32, (void *)At, 5, da, sa, ba, false);
+        const uint64_t db[3] = {(uint64_t)Wn, (uint64_t)b.l, (uint64_t)b.nprob};
+        const uint64_t sbb[2] = {(uint64_t)pb * 8, (uint64_t)(b.nprob > 1 ? sb : b.l * pb) * 8};
+        const uint32_t bb[3] = {(uint32_t)kTileWords, 32, 1};
+        if (rc == GF2_OK) rc = encode_map_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT64, (void *)Bm, db, sbb, bb, false);
+    } else if (rc == GF2_OK) {
         // A^T: rows x words x problems (DIRECT, A: words x rows x problems);
         // B: words x rows x problems
         const uint32_t abox = (uint32_t)std::min(kThreads * rpt, 256);
@@ -588,7 +909,22 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     if (rc == GF2_OK) {
         const int64_t z = (int64_t)nsplit * b.nprob;
         const int tidx = timer_begin(s, (double)b.m * (double)b.l * (double)b.n * (double)b.nprob);
-        if (rpt == 8)
+        if (rpt == 16) {
+            static bool configured[64] = {};
+            if (first_on_device(configured))
+                rc = check_cuda(cudaFuncSetAttribute(k_m4rm_tm, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmSmem),
+                                "cudaFuncSetAttribute(k_m4rm_tm)");
+            if (rc == GF2_OK) {
+                dim3 grid((unsigned)col_tiles, (unsigned)row_tiles, (unsigned)z);
+                const cudaError_t le = launch_k(k_m4rm_tm, grid, kThreads, kTmSmem, s, 1, ka, ta, tb);
+                rc = le == cudaSuccess ? check_cuda(cudaGetLastError(), "k_m4rm_tm launch")
+                                       : check_cuda(le, "k_m4rm_tm launch");
+                if (rc == GF2_OK) {
+                    note_launch();
+                    g_m4rm_launches.fetch_add(1, std::memory_order_relaxed);
+                }
+            }
+        } else if (rpt == 8)
             rc = launch_rpt<8, false>(ka, ta, tb, col_tiles, row_tiles, z, s);
         else if (rpt == 4)
             rc = direct ? launch_rpt<4, true>(ka, ta, tb, col_tiles, row_tiles, z, s)

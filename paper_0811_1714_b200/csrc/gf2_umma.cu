@@ -344,13 +344,13 @@ namespace {
 // buffers (serving, benchmarks, recursion levels) skips the driver's
 // encode on the host path; a hit is a 128-byte copy.
 struct MapKey {
-    int dt;
+    int dt, rank;
     void *base;
-    uint64_t dims[3], strides[2];
-    uint32_t box[3];
+    uint64_t dims[5], strides[4];
+    uint32_t box[5];
     bool swz;
     bool operator==(const MapKey &o) const {
-        return dt == o.dt && base == o.base && swz == o.swz && !memcmp(dims, o.dims, sizeof dims) &&
+        return dt == o.dt && rank == o.rank && base == o.base && swz == o.swz && !memcmp(dims, o.dims, sizeof dims) &&
                !memcmp(strides, o.strides, sizeof strides) && !memcmp(box, o.box, sizeof box);
     }
 };
@@ -364,27 +364,45 @@ thread_local MapEntry t_maps[kMapCache];
 thread_local int t_next = 0;
 }  // namespace
 
-int encode_map_3d(CUtensorMap *map, CUtensorMapDataType dt, void *base, const uint64_t dims[3],
-                  const uint64_t strides[2], const uint32_t box[3], bool swizzle128) {
-    MapKey key{(int)dt, base, {dims[0], dims[1], dims[2]}, {strides[0], strides[1]}, {box[0], box[1], box[2]},
-               swizzle128};
+int encode_map_nd(CUtensorMap *map, CUtensorMapDataType dt, void *base, int rank, const uint64_t *dims,
+                  const uint64_t *strides, const uint32_t *box, bool swizzle128) {
+    if (rank < 1 || rank > 5) return set_error(GF2_ERR_INTERNAL, "tensor map rank");
+    MapKey key{};
+    key.dt = (int)dt;
+    key.rank = rank;
+    key.base = base;
+    key.swz = swizzle128;
+    for (int i = 0; i < rank; ++i) {
+        key.dims[i] = dims[i];
+        key.box[i] = box[i];
+        if (i + 1 < rank) key.strides[i] = strides[i];
+    }
     for (int i = 0; i < kMapCache; ++i)
         if (t_maps[i].used && t_maps[i].k == key) {
             *map = t_maps[i].m;
             return GF2_OK;
         }
     GF2_TRY(get_encode());
-    cuuint64_t d[3] = {dims[0], dims[1], dims[2]};
-    cuuint64_t st[2] = {strides[0], strides[1]};
-    cuuint32_t bx[3] = {box[0], box[1], box[2]};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = g_encode(map, dt, 3, base, d, st, bx, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    cuuint64_t d[5], st[4];
+    cuuint32_t bx[5], estr[5];
+    for (int i = 0; i < rank; ++i) {
+        d[i] = dims[i];
+        bx[i] = box[i];
+        estr[i] = 1;
+        if (i + 1 < rank) st[i] = strides[i];
+    }
+    CUresult r = g_encode(map, dt, (cuuint32_t)rank, base, d, st, bx, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                           swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_error(GF2_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
     t_maps[t_next] = MapEntry{key, *map, true};
     t_next = (t_next + 1) % kMapCache;
     return GF2_OK;
+}
+
+int encode_map_3d(CUtensorMap *map, CUtensorMapDataType dt, void *base, const uint64_t dims[3],
+                  const uint64_t strides[2], const uint32_t box[3], bool swizzle128) {
+    return encode_map_nd(map, dt, base, 3, dims, strides, box, swizzle128);
 }
 
 int launch_expand(const ExpandArgs &a, int64_t nprob, cudaStream_t s) {
