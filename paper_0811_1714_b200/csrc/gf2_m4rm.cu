@@ -761,11 +761,11 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     auto zero_c = [&]() -> int {
         if (b.nprob == 1 || b.sc == b.m * b.pc) {
             gf2_view v{b.C, b.pc, b.m * b.nprob, b.n};
-            return launch_ewise(v, nullptr, nullptr, 0, s);
+            return launch_zero(v, s);  // a 2-D memset when whole words
         }
         for (int64_t q = 0; q < b.nprob; ++q) {
             gf2_view v{b.C + q * b.sc, b.pc, b.m, b.n};
-            GF2_TRY(launch_ewise(v, nullptr, nullptr, 0, s));
+            GF2_TRY(launch_zero(v, s));
         }
         return GF2_OK;
     };
