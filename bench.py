@@ -375,7 +375,7 @@ def launch_ranks(args) -> int:
     """--gpus N > 1 without torchrun: re-launch this script as N ranks (one
     process per GPU) through torch.distributed.run on 127.0.0.1. Refuses
     (exit 2) when fewer than N CUDA devices are visible."""
-    if args.impl == "b200":
+    if args.impl == "b200" and not os.environ.get("GF2_BENCH_SHARE_GPU"):
         import torch
         have = torch.cuda.device_count()
         if have < args.gpus:
@@ -448,15 +448,17 @@ def digest_rows(ctx, out, w):
     import torch.distributed as dist
     from paper_0811_1714_b200.sharded import shard_rows
     width = g.words_per_row(w["n"])
+    cuda_p2p = dist.get_backend() == "nccl"  # gloo (GF2_BENCH_SHARE_GPU) sends host tensors
     h = hashlib.sha256() if ctx.rank == 0 else None
     for r in range(ctx.world):
         r0, r1 = shard_rows(w["m"], ctx.world, r)
         if r == ctx.rank == 0:
             h.update(out.to_numpy().astype("<u8", copy=False).tobytes())
         elif r == ctx.rank:
-            dist.send(out.storage[:, :width].contiguous(), dst=0)
+            t = out.storage[:, :width].contiguous()
+            dist.send(t if cuda_p2p else t.cpu(), dst=0)
         elif ctx.rank == 0:
-            t = torch.empty((r1 - r0, width), dtype=torch.int64, device=ctx.dev)
+            t = torch.empty((r1 - r0, width), dtype=torch.int64, device=ctx.dev if cuda_p2p else "cpu")
             dist.recv(t, src=r)
             h.update(t.cpu().numpy().tobytes())
     return h.hexdigest() if ctx.rank == 0 else None
@@ -899,6 +901,12 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # GF2_BENCH_SHARE_GPU=1 (tests only): every rank on cuda:0 with gloo for
+    # the collectives, to run the N > 1 code path on a one-GPU box; the
+    # numbers it prints are not a measurement and the line says so
+    share = bool(os.environ.get("GF2_BENCH_SHARE_GPU"))
+    if share:
+        local = 0
     ndev = torch.cuda.device_count()
     if local >= ndev:
         die(f"rank {rank}: LOCAL_RANK {local} but {ndev} CUDA device(s) visible")
@@ -912,7 +920,10 @@ def run_b200(args):
             os.environ.setdefault("WORLD_SIZE", "1")
         else:
             os.environ.setdefault("NCCL_DEBUG", "INFO")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         if dist.get_world_size() != args.gpus and not (args.sharded and world == 1):
             die(f"process group has {dist.get_world_size()} ranks, --gpus {args.gpus}")
     dev = torch.device("cuda", local)
@@ -937,6 +948,8 @@ def run_b200(args):
                 "scaling": "strong", "vs_baseline": None, "dtype": "u64",
                 "engine": args.engine}
         line.update(_line_part(ctx, main_res))
+        if share:
+            line["share_gpu_test"] = "all ranks on cuda:0 over gloo: a code-path test, not a measurement"
         line["compute"] = {
             "tc-f4": "GF(2) words as u64 (XOR additions); leaf products as "
                      "e2m1 nibbles x e2m1 -> f32 (tcgen05 kind::mxf4, exact "

@@ -1,0 +1,36 @@
+"""bench.py's N > 1 path end to end on a one-GPU box: `--gpus 2` self-launches
+two ranks through torch.distributed.run; with GF2_BENCH_SHARE_GPU=1 (a
+test-only switch) both ranks run on cuda:0 with gloo for the collectives
+instead of NCCL. Row shards of A and C, the K-panel broadcast of B, the
+max-over-ranks timing, the rank-ordered digest of the gathered C and the
+sharded host pipeline all run as they would on two GPUs; the line must be
+digest-verified and flagged as a code-path test, not a measurement."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_bench_two_ranks_share_one_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, GF2_BENCH_SHARE_GPU="1")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2",
+                          "--warmup", "1", "--extra", "none", "--no-cpu-baseline"],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["verified_sha256"] is True
+    assert "share_gpu_test" in d
+    assert d["e2e"]["verified_vs_device_result"] is True
+    assert d["config"]["parallelism"].startswith("rows2")
