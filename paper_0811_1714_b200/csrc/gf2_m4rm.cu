@@ -779,11 +779,15 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     // words 8 KiB per RPT (TMA write + LDS), the table build ~82 KiB
     // whatever the tile height (8 tables x 256 slots x 32 B of stores plus
     // the source rows). A CTA runs its K range plus a fixed cost (launch,
-    // pipeline fill, epilogue) of about half a word; CTAs run in waves of
+    // pipeline fill, first table builds, epilogue) of about two words --
+    // fitted to the 7 batched 8192^3 leaves of cfg3 on the M4RM engine
+    // (RPT 16: 4/5/7/8/13 splits measured 2.335/2.187/2.216/2.302/2.341 ms;
+    // with half a word the model picked 13) -- and CTAs run in waves of
     // one per SM. A K split also costs the zeroing pass and red.xor. Large
-    // products keep RPT 8 (BM 4096) and split K only to fill waves (16384^3:
-    // 256 tiles, 4 splits, 6.92 waves); small ones (cfg1 1024^3) trade
-    // taller tiles for more CTAs with shorter K ranges.
+    // products take RPT 16 (BM 8192, half the rows parked in TMEM) and split
+    // K only to fill waves (16384^3: 128 tiles, 8 splits, 6.92 waves); small
+    // ones (cfg1 1024^3) trade taller tiles for more CTAs with shorter K
+    // ranges.
     int rpt = 8;
     int nsplit = 1;
     int64_t kws = Wl;
@@ -798,7 +802,7 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
                 if (ns != n) continue;
                 const int64_t ctas = tiles * ns;
                 const int64_t waves = (ctas + sms - 1) / sms;
-                const double per_cta = ((double)w + 0.5) * (82.0 + 136.0 * r);
+                const double per_cta = ((double)w + 2.0) * (82.0 + 136.0 * r);
                 const double cost = (double)waves * per_cta * (ns > 1 ? 1.02 : 1.0);
                 if (best == 0 || cost < best * 0.999) {
                     best = cost;
@@ -821,6 +825,12 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
         }
     }
     const int64_t row_tiles = (b.m + kThreads * rpt - 1) / (kThreads * rpt);
+    {
+        static const bool verbose = getenv("GF2_M4RM_VERBOSE") != nullptr;  // tools/ only
+        if (verbose)
+            fprintf(stderr, "k_m4rm geometry: m=%lld l=%lld n=%lld nprob=%lld -> rpt=%d nsplit=%d kws=%lld\n",
+                    (long long)b.m, (long long)b.l, (long long)b.n, (long long)b.nprob, rpt, nsplit, (long long)kws);
+    }
     if ((int64_t)nsplit * b.nprob > 65535 || row_tiles > 65535 || col_tiles > 2147483647)
         return set_error(GF2_ERR_PARAMETER, "m4rm grid too large");
     if (b.m > 2147483647 || b.l > 2147483647 / 2)
