@@ -456,6 +456,26 @@ __global__ void __launch_bounds__(256) k_words_th(const u64 *A, int64_t pa, int6
     }
 }
 
+// 4-row register groups (32 accumulator words) <-> 32 TMEM columns
+__device__ __forceinline__ void tm_swap32(uint32_t st_addr, uint32_t ld_addr, uint32_t (&x)[4][8]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%32], {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31};\n"
+        "tcgen05.wait::st.sync.aligned;\n"
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%33];\n"
+        "tcgen05.wait::ld.sync.aligned;\n"
+        : "+r"(x[0][0]), "+r"(x[0][1]), "+r"(x[0][2]), "+r"(x[0][3]), "+r"(x[0][4]), "+r"(x[0][5]), "+r"(x[0][6]), "+r"(x[0][7]), "+r"(x[1][0]), "+r"(x[1][1]), "+r"(x[1][2]), "+r"(x[1][3]), "+r"(x[1][4]), "+r"(x[1][5]), "+r"(x[1][6]), "+r"(x[1][7]), "+r"(x[2][0]), "+r"(x[2][1]), "+r"(x[2][2]), "+r"(x[2][3]), "+r"(x[2][4]), "+r"(x[2][5]), "+r"(x[2][6]), "+r"(x[2][7]), "+r"(x[3][0]), "+r"(x[3][1]), "+r"(x[3][2]), "+r"(x[3][3]), "+r"(x[3][4]), "+r"(x[3][5]), "+r"(x[3][6]), "+r"(x[3][7])
+        : "r"(st_addr), "r"(ld_addr)
+        : "memory");
+}
+__device__ __forceinline__ void tm_store32(uint32_t taddr, const uint32_t (&x)[4][8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};\n" ::"r"(taddr), "r"(x[0][0]), "r"(x[0][1]), "r"(x[0][2]), "r"(x[0][3]), "r"(x[0][4]), "r"(x[0][5]), "r"(x[0][6]), "r"(x[0][7]), "r"(x[1][0]), "r"(x[1][1]), "r"(x[1][2]), "r"(x[1][3]), "r"(x[1][4]), "r"(x[1][5]), "r"(x[1][6]), "r"(x[1][7]), "r"(x[2][0]), "r"(x[2][1]), "r"(x[2][2]), "r"(x[2][3]), "r"(x[2][4]), "r"(x[2][5]), "r"(x[2][6]), "r"(x[2][7]), "r"(x[3][0]), "r"(x[3][1]), "r"(x[3][2]), "r"(x[3][3]), "r"(x[3][4]), "r"(x[3][5]), "r"(x[3][6]), "r"(x[3][7]) : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tm_load32(uint32_t taddr, uint32_t (&x)[4][8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n" : "=r"(x[0][0]), "=r"(x[0][1]), "=r"(x[0][2]), "=r"(x[0][3]), "=r"(x[0][4]), "=r"(x[0][5]), "=r"(x[0][6]), "=r"(x[0][7]), "=r"(x[1][0]), "=r"(x[1][1]), "=r"(x[1][2]), "=r"(x[1][3]), "=r"(x[1][4]), "=r"(x[1][5]), "=r"(x[1][6]), "=r"(x[1][7]), "=r"(x[2][0]), "=r"(x[2][1]), "=r"(x[2][2]), "=r"(x[2][3]), "=r"(x[2][4]), "=r"(x[2][5]), "=r"(x[2][6]), "=r"(x[2][7]), "=r"(x[3][0]), "=r"(x[3][1]), "=r"(x[3][2]), "=r"(x[3][3]), "=r"(x[3][4]), "=r"(x[3][5]), "=r"(x[3][6]), "=r"(x[3][7]) : "r"(taddr) : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     k_m4rm_tm(KArgs p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -567,23 +587,26 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     // accumulators of the register group: row i, u32 words 0..3 = slice par,
     // 4..7 = slice 1-par; the other group parked at TMEM columns slot*64
-    uint32_t acc[8][8];
+    // 4 groups of 4 rows (rows g*2048 + i*512 + tid): one group in
+    // registers (32 words), three parked at TMEM columns g*32
+    uint32_t acc[4][8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[i][e] = 0;
     const uint32_t tlane = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 128);
-    tm_store(tlane + 64, acc);  // group 1 starts at zero
+#pragma unroll 1
+    for (int g = 1; g < 4; ++g) tm_store32(tlane + g * 32, acc);  // parked groups start at zero
     int cur = 0;
 
     const int pair = warp >> 1;
     if (pair == 0 && H > 0) build(0);
     if (pair == 1 && H > 1) build(1);
 
-    auto lookups = [&](uint32_t tb, const uint32_t (&a)[8]) {
+    auto lookups = [&](uint32_t tb, const uint32_t (&a)[4]) {
         const uint32_t tq = s_tab + tb + (par << 4);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < 4; ++i) {
             const uint32_t hw = a[i];
             const uint32_t r = __funnelshift_l(hw, hw, 8 * q);  // byte 3-t <-> table (q+t)&3
 #pragma unroll
@@ -598,22 +621,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     };
 
-    uint32_t a[8];
+    uint32_t a[4];
     for (int h = 0; h < H; ++h) {
         const int slot = h % kNT;
         const uint32_t sa = s_a + (h % kTmNA) * kTmA + tid * 4;
         mbar_wait(b_tfull + 8 * slot, (h / kNT) & 1);
         mbar_wait(b_afull + 8 * (h % kTmNA), (h / kTmNA) & 1);
         const uint32_t tb = slot * kTabBytes;
+#pragma unroll 1
+        for (int step = 0; step < 4; ++step) {
+            if (step) {
+                const int nxt = (cur + 1) & 3;
+                tm_swap32(tlane + cur * 32, tlane + nxt * 32, acc);
+                cur = nxt;
+            }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) a[i] = lds32(sa + (cur * 4096 + i * kThreads) * 4);
-        lookups(tb, a);
-        tm_swap(tlane + cur * 64, tlane + (cur ^ 1) * 64, acc);
-        cur ^= 1;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) a[i] = lds32(sa + (cur * 4096 + i * kThreads) * 4);
-        warp_arrive(b_aempty + 8 * (h % kTmNA), lane);
-        lookups(tb, a);
+            for (int i = 0; i < 4; ++i) a[i] = lds32(sa + (cur * 2048 + i * kThreads) * 4);
+            if (step == 3) warp_arrive(b_aempty + 8 * (h % kTmNA), lane);
+            lookups(tb, a);
+        }
         warp_arrive(b_tempty + 8 * slot, lane);
         if (tid == 0) {
             // A slot of half-word h-1 takes h+2 once every warp has read it;
@@ -632,14 +658,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const u64 ntm = tail_mask(p.n);
     const int64_t row0 = (int64_t)rb0 * 256;
 #pragma unroll 1
-    for (int pass = 0; pass < 2; ++pass) {
+    for (int pass = 0; pass < 4; ++pass) {
         if (pass) {
-            cur ^= 1;
-            tm_load(tlane + cur * 64, acc);
+            cur = (cur + 1) & 3;
+            tm_load32(tlane + cur * 32, acc);
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int64_t row = row0 + cur * 4096 + i * kThreads + tid;
+        for (int i = 0; i < 4; ++i) {
+            const int64_t row = row0 + cur * 2048 + i * kThreads + tid;
             if (row >= p.m) continue;
             u64 *crow = C + row * p.pc;
 #pragma unroll
