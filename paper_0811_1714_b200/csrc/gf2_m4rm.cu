@@ -374,12 +374,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Stages are one A half-word (32 KiB of the half-word-major A^T, one 5-D TMA
 // box) in a 3-slot ring, B half panels (1 KiB) in an 8-slot ring, and the
 // 3-slot half-word table ring of k_m4rm.
-constexpr int kTmRows = 8192;
-constexpr int kTmA = kTmRows * 4;   // one A half-word for 8192 rows
+// NG groups of 4 rows per thread (NG = 2..4): BM = 2048 NG rows per CTA
+template <int NG>
+constexpr int tm_rows() {
+    return 2048 * NG;
+}
+template <int NG>
+constexpr int tm_stage_a() {
+    return tm_rows<NG>() * 4;  // one A half-word for BM rows
+}
 constexpr int kTmNA = 3;
 constexpr int kTmNB = 8;
 constexpr int kTmB = 32 * 32;       // 32 rows x 32 B
-constexpr int kTmSmem = kNT * kTabBytes + kTmNA * kTmA + kTmNB * kTmB + 256;
+template <int NG>
+constexpr int tm_smem() {
+    return kNT * kTabBytes + kTmNA * tm_stage_a<NG>() + kTmNB * kTmB + 256;
+}
 
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
     uint32_t v;
@@ -476,8 +486,11 @@ __device__ __forceinline__ void tm_load32(uint32_t taddr, uint32_t (&x)[4][8]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
+template <int NG>
 __global__ void __launch_bounds__(kThreads, 1)
     k_m4rm_tm(KArgs p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
+    constexpr int kTmRows = tm_rows<NG>();
+    constexpr int kTmA = tm_stage_a<NG>();
     extern __shared__ __align__(1024) unsigned char smem[];
     const uint32_t s_tab = (uint32_t)__cvta_generic_to_shared(smem);
     const uint32_t s_a = s_tab + kNT * kTabBytes;
@@ -596,7 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int e = 0; e < 8; ++e) acc[i][e] = 0;
     const uint32_t tlane = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 128);
 #pragma unroll 1
-    for (int g = 1; g < 4; ++g) tm_store32(tlane + g * 32, acc);  // parked groups start at zero
+    for (int g = 1; g < NG; ++g) tm_store32(tlane + g * 32, acc);  // parked groups start at zero
     int cur = 0;
 
     const int pair = warp >> 1;
@@ -629,15 +642,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(b_afull + 8 * (h % kTmNA), (h / kTmNA) & 1);
         const uint32_t tb = slot * kTabBytes;
 #pragma unroll 1
-        for (int step = 0; step < 4; ++step) {
+        for (int step = 0; step < NG; ++step) {
             if (step) {
-                const int nxt = (cur + 1) & 3;
+                const int nxt = cur + 1 == NG ? 0 : cur + 1;
                 tm_swap32(tlane + cur * 32, tlane + nxt * 32, acc);
                 cur = nxt;
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i) a[i] = lds32(sa + (cur * 2048 + i * kThreads) * 4);
-            if (step == 3) warp_arrive(b_aempty + 8 * (h % kTmNA), lane);
+            if (step == NG - 1) warp_arrive(b_aempty + 8 * (h % kTmNA), lane);
             lookups(tb, a);
         }
         warp_arrive(b_tempty + 8 * slot, lane);
@@ -658,9 +671,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const u64 ntm = tail_mask(p.n);
     const int64_t row0 = (int64_t)rb0 * 256;
 #pragma unroll 1
-    for (int pass = 0; pass < 4; ++pass) {
+    for (int pass = 0; pass < NG; ++pass) {
         if (pass) {
-            cur = (cur + 1) & 3;
+            cur = cur + 1 == NG ? 0 : cur + 1;
             tm_load32(tlane + cur * 32, acc);
         }
 #pragma unroll
@@ -691,6 +704,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase) : "memory");
     }
+}
+
+template <int NG>
+int launch_tm(const KArgs &ka, const CUtensorMap &ta, const CUtensorMap &tb, dim3 grid, cudaStream_t s) {
+    static bool configured[64] = {};
+    if (first_on_device(configured))
+        GF2_TRY(check_cuda(cudaFuncSetAttribute(k_m4rm_tm<NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                tm_smem<NG>()),
+                           "cudaFuncSetAttribute(k_m4rm_tm)"));
+    GF2_LAUNCH(launch_k(k_m4rm_tm<NG>, grid, kThreads, tm_smem<NG>(), s, 1, ka, ta, tb));
+    note_launch();
+    g_m4rm_launches.fetch_add(1, std::memory_order_relaxed);
+    return check_cuda(cudaGetLastError(), "k_m4rm_tm launch");
 }
 
 template <int RPT, bool DIRECT>
@@ -819,7 +845,7 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     int64_t kws = Wl;
     {
         double best = 0;
-        for (int r : {16, 8, 4, 2, 1}) {
+        for (int r : {16, 12, 8, 4, 2, 1}) {
             const int64_t rt = (b.m + kThreads * r - 1) / (kThreads * r);
             const int64_t tiles = rt * col_tiles * b.nprob;
             for (int64_t n = 1; n <= 16 && n <= Wl; ++n) {
@@ -843,7 +869,7 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
         // tuning override, GF2_M4RM_GEOM="rpt,nsplit" (tools/ only)
         static const char *geom = getenv("GF2_M4RM_GEOM");
         int r = 0, n = 0;
-        if (geom && sscanf(geom, "%d,%d", &r, &n) == 2 && (r == 1 || r == 2 || r == 4 || r == 8 || r == 16) && n >= 1 &&
+        if (geom && sscanf(geom, "%d,%d", &r, &n) == 2 && (r == 1 || r == 2 || r == 4 || r == 8 || r == 12 || r == 16) && n >= 1 &&
             n <= 16) {
             rpt = r;
             kws = (Wl + n - 1) / n;
@@ -869,7 +895,7 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     GF2_TRY(pool_setup());
     const bool direct = rpt <= 4 && (uintptr_t)b.A % 16 == 0 && b.pa % 2 == 0 && (b.nprob == 1 || b.sa % 2 == 0) &&
                         b.m * Wl * b.nprob <= (int64_t(1) << 20);
-    const bool tm = rpt == 16;  // BM 8192, TMEM-parked rows, half-word-major A^T
+    const bool tm = rpt >= 8;  // BM 4096..8192, TMEM-parked row groups, half-word-major A^T
     const int64_t mp = tm ? (b.m + 255) & ~int64_t(255) : (b.m + 1) & ~int64_t(1);
     const bool b_ok = ((uintptr_t)b.B % 16 == 0) && (b.pb % 2 == 0) && (b.nprob == 1 || b.sb % 2 == 0);
     const int64_t wnp = (Wn + 1) & ~int64_t(1);
@@ -913,7 +939,7 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
         // A^T half-word-major (u32): 256 rows x row blocks x halves x words x problems
         const uint64_t da[5] = {256, (uint64_t)(mp / 256), 2, (uint64_t)Wl, (uint64_t)b.nprob};
         const uint64_t sa[4] = {1024, (uint64_t)mp * 4, (uint64_t)mp * 8, (uint64_t)(Wl * mp) * 8};
-        const uint32_t ba[5] = {256, kTmRows / 256, 1, 1, 1};
+        const uint32_t ba[5] = {256, (uint32_t)(kThreads * rpt / 256), 1, 1, 1};
         rc = encode_map_nd(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT32, (void *)At, 5, da, sa, ba, false);
         const uint64_t db[3] = {(uint64_t)Wn, (uint64_t)b.l, (uint64_t)b.nprob};
         const uint64_t sbb[2] = {(uint64_t)pb * 8, (uint64_t)(b.nprob > 1 ? sb : b.l * pb) * 8};
@@ -945,24 +971,11 @@ int launch_m4rm(const M4rmBatch &b, cudaStream_t s) {
     if (rc == GF2_OK) {
         const int64_t z = (int64_t)nsplit * b.nprob;
         const int tidx = timer_begin(s, (double)b.m * (double)b.l * (double)b.n * (double)b.nprob);
-        if (rpt == 16) {
-            static bool configured[64] = {};
-            if (first_on_device(configured))
-                rc = check_cuda(cudaFuncSetAttribute(k_m4rm_tm, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmSmem),
-                                "cudaFuncSetAttribute(k_m4rm_tm)");
-            if (rc == GF2_OK) {
-                dim3 grid((unsigned)col_tiles, (unsigned)row_tiles, (unsigned)z);
-                const cudaError_t le = launch_k(k_m4rm_tm, grid, kThreads, kTmSmem, s, 1, ka, ta, tb);
-                rc = le == cudaSuccess ? check_cuda(cudaGetLastError(), "k_m4rm_tm launch")
-                                       : check_cuda(le, "k_m4rm_tm launch");
-                if (rc == GF2_OK) {
-                    note_launch();
-                    g_m4rm_launches.fetch_add(1, std::memory_order_relaxed);
-                }
-            }
-        } else if (rpt == 8)
-            rc = launch_rpt<8, false>(ka, ta, tb, col_tiles, row_tiles, z, s);
-        else if (rpt == 4)
+        if (tm) {
+            dim3 grid((unsigned)col_tiles, (unsigned)row_tiles, (unsigned)z);
+            rc = rpt == 16 ? launch_tm<4>(ka, ta, tb, grid, s)
+                           : (rpt == 12 ? launch_tm<3>(ka, ta, tb, grid, s) : launch_tm<2>(ka, ta, tb, grid, s));
+        }        else if (rpt == 4)
             rc = direct ? launch_rpt<4, true>(ka, ta, tb, col_tiles, row_tiles, z, s)
                         : launch_rpt<4, false>(ka, ta, tb, col_tiles, row_tiles, z, s);
         else if (rpt == 2)

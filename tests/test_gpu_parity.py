@@ -428,9 +428,9 @@ print("BAD", bad)
 """
 
 
-@pytest.mark.parametrize("geom", ["16,1", "16,5", "8,1", "8,3", "4,5", "2,16", "1,8", "1,16"])
+@pytest.mark.parametrize("geom", ["16,1", "16,5", "12,2", "8,1", "8,3", "4,5", "2,16", "1,8", "1,16"])
 def test_m4rm_every_geometry(geom):
-    """Every k_m4rm tile height (RPT 16/8/4/2/1 -> 8192 (TMEM-parked)/4096/2048/1024/512 rows) and
+    """Every k_m4rm tile height (RPT 16/12/8 -> 8192/6144/4096 rows with TMEM-parked groups, 4/2/1 -> 2048/1024/512) and
     K-split count, forced through GF2_M4RM_GEOM (read once per process,
     hence a subprocess), on ragged shapes with the TMA path (aligned
     operands), the 8-byte cp.async path (odd word offsets) and both mixes,

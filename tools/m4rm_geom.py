@@ -18,6 +18,7 @@ from oracle import gf2_oracle as O  # noqa: E402
 
 m, l, n = (int(x) for x in sys.argv[1:4])
 torch.cuda.set_device(0)
+g.set_engine("m4rm")  # the M4RM kernel itself, whatever the size
 a, b = g.random(m, l, 1), g.random(l, n, 2)
 c = g.mul_m4rm(a, b, 8)
 torch.cuda.synchronize()
