@@ -168,7 +168,7 @@ struct UArgs {
     int post;
     int64_t qoffC[4];
     unsigned post_mask[7];
-    int dbg;  // timing experiments only (GF2_F4_DBG): 1 no C stores, 2 no epilogue work
+    int dbg;  // timing experiments only (GF2_F4_DBG / GF2_UMMA_DBG): 1 no C stores, 2 no epilogue work
     int order;  // tile raster (GF2_F4_ORDER): 0 column tiles fastest, G > 0 blocks of G row tiles
 };
 

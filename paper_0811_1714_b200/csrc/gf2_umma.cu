@@ -267,6 +267,14 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
             const uint32_t acc_phase = (it >> 1) & 1;
             mbar_wait(bar_tfull + 8 * acc, acc_phase);
             tc_fence_after();
+            if (p.dbg == 2) {  // timing only (GF2_UMMA_DBG=2): operand TMA + MMAs, no epilogue work
+                tc_fence_before();
+                if (CG == 1)
+                    mbar_arrive(bar_tempty + 8 * acc);
+                else
+                    mbar_arrive_leader(bar_tempty + 8 * acc);
+                continue;
+            }
             uint32_t packed[BN / 32];
 #pragma unroll
             for (int c = 0; c < BN / 32; ++c) {
@@ -510,6 +518,8 @@ int launch_umma_job(const UmmaJob &jb, int kind, cudaStream_t s) {
     ua.kchunk_blocks = kind == 0 ? ua.kblocks : (int)(F8_KCHUNK / BK);
     ua.nchunks = (ua.kblocks + ua.kchunk_blocks - 1) / ua.kchunk_blocks;
     ua.post = jb.fuse_post;
+    static const int udbg = getenv("GF2_UMMA_DBG") ? atoi(getenv("GF2_UMMA_DBG")) : 0;
+    ua.dbg = udbg;
     int rc = GF2_OK;
     if (jb.fuse_post) {
         ua.qoffC[0] = 0;

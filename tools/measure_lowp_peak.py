@@ -6,10 +6,11 @@ bf16 only). Writes profiles/measured_peaks_lowp.json.
     `torch._scaled_mm`, int8 `torch._int_mm`, fp8 e4m3 `torch._scaled_mm`,
     N^3 at N = 8192 and 16384; burst = best of 20 single calls (CUDA
     events), sustained = back to back for 3 s; 2 ops per MAC.
-  * this repo's k_umma_f4 with its epilogue switched off (GF2_F4_DBG=2:
-    operand TMA + MMAs only, a timing-only knob) on a direct 8192^3 and on
-    the 7 batched 8192^3 leaves of cfg3, timed by the library's kernel
-    timer -- the MMA issue rate the product kernel itself can reach.
+  * this repo's k_umma_f4 / k_umma (i8, f8) with the epilogue switched off
+    (GF2_F4_DBG=2 / GF2_UMMA_DBG=2: operand TMA + MMAs only, timing-only
+    knobs) on a direct 8192^3 and on the 7 batched 8192^3 leaves of cfg3,
+    timed by the library's kernel timer -- the MMA rate the product kernels
+    themselves can reach.
 
 NVML SM clocks are sampled every 5 ms during each timed region.
 
@@ -33,7 +34,7 @@ sys.path.insert(0, %(root)r)
 import paper_0811_1714_b200 as g
 from paper_0811_1714_b200 import _lib
 torch.cuda.set_device(0)
-g.set_engine("tc-f4")
+g.set_engine(%(engine)r)
 out = {}
 for name, fn in (("direct_8192", None), ("cfg3_leaves", None)):
     if name == "direct_8192":
@@ -183,13 +184,15 @@ def main():
             torch.cuda.empty_cache()
         del bits_a, bits_b, pa, pb, a8, b8, af8, bf8
         torch.cuda.empty_cache()
-    env = dict(os.environ, GF2_F4_DBG="2")
-    p = subprocess.run([sys.executable, "-c", MMA_ONLY % {"root": ROOT}], env=env, capture_output=True, text=True,
-                       timeout=600)
-    try:
-        res["k_umma_f4_mma_only_tflops"] = json.loads(p.stdout.strip().splitlines()[-1])
-    except Exception:
-        res["k_umma_f4_mma_only_error"] = (p.stdout + p.stderr)[-600:]
+    for engine, key in (("tc-f4", "k_umma_f4_mma_only_tflops"), ("tc-i8", "k_umma_i8_mma_only_tops"),
+                        ("tc-f8", "k_umma_f8_mma_only_tflops")):
+        env = dict(os.environ, GF2_F4_DBG="2", GF2_UMMA_DBG="2")
+        p = subprocess.run([sys.executable, "-c", MMA_ONLY % {"root": ROOT, "engine": engine}], env=env,
+                           capture_output=True, text=True, timeout=600)
+        try:
+            res[key] = json.loads(p.stdout.strip().splitlines()[-1])
+        except Exception:
+            res[key.replace("tflops", "error").replace("tops", "error")] = (p.stdout + p.stderr)[-600:]
 
     def best(prefix):
         vals = [v.get("burst_tflops", 0) for k, v in res["cublas"].items() if k.startswith(prefix)]
@@ -198,10 +201,11 @@ def main():
     f4 = [best("mxf4_")] + list(res.get("k_umma_f4_mma_only_tflops", {}).values())
     f4 = [x for x in f4 if x]
     res["mxf4_tflops"] = max(f4) if f4 else None
-    res["i8_tops"] = best("i8_")
-    res["f8_tflops"] = best("f8_")
-    res["how"] = ("max over cuBLASLt burst (best of 20, N^3 at N=8192/16384, 2 ops/MAC) and, for mxf4, "
-                  "k_umma_f4 with the epilogue off (GF2_F4_DBG=2) timed by the library's kernel timer")
+    res["i8_tops"] = max([best("i8_") or 0] + list(res.get("k_umma_i8_mma_only_tops", {}).values()))
+    res["f8_tflops"] = max([best("f8_") or 0] + list(res.get("k_umma_f8_mma_only_tflops", {}).values()))
+    res["how"] = ("max over cuBLASLt burst (best of 20, N^3 at N=8192/16384, 2 ops/MAC) and this library's "
+                  "GEMMs with the epilogue off (GF2_F4_DBG=2 / GF2_UMMA_DBG=2: operand TMA + MMAs) timed by its "
+                  "kernel timer, on a direct 8192^3 and on cfg3's 7 batched 8192^3 leaves")
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     with open(OUT, "w") as fh:
         json.dump(res, fh, indent=1)
