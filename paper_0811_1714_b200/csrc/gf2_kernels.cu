@@ -244,6 +244,11 @@ __global__ void __launch_bounds__(256) k_combine_t(CombineArgs p) {
     const int ngroups = (int)min((int64_t)(CT_ROWS / 64), (p.R - r0 + 63) / 64);
     const bool vec = ngroups == 4 && (p.dst_pitch % 2 == 0) && (p.dst_stride % 2 == 0);
     u64 *db = p.dst + (int64_t)blockIdx.z * 7 * p.dst_stride;
+    // one 32-byte store (STG.256) per transposed row and output when the rows
+    // are sector aligned: a whole sector per lane instead of two half-sector
+    // writes (ncu: 32 sectors per 16-byte store request, each written twice)
+    const bool vec32 = vec && (p.dst_pitch % 4 == 0) && (p.dst_stride % 4 == 0) &&
+                       ((uintptr_t)db % 32 == 0);
 #pragma unroll 1
     for (int half = 0; half < 2; ++half) {
         u64 T[4][NG];  // [quadrant][64-row group]: transposed word of row 64w + 32 half + lane
@@ -269,7 +274,11 @@ __global__ void __launch_bounds__(256) k_combine_t(CombineArgs p) {
                     if (p.mask[q] & (1u << qd)) o[g] ^= T[qd][g];
             }
             u64 *drow = db + q * p.dst_stride + orow * p.dst_pitch + r0 / 64;
-            if (NG == 4 && vec) {
+            if (NG == 4 && vec32) {
+                asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(drow), "l"(o[0]),
+                             "l"(o[NG > 1 ? 1 : 0]), "l"(o[NG > 2 ? 2 : 0]), "l"(o[NG > 3 ? 3 : 0])
+                             : "memory");
+            } else if (NG == 4 && vec) {
                 reinterpret_cast<ulonglong2 *>(drow)[0] = make_ulonglong2(o[0], o[NG > 1 ? 1 : 0]);
                 reinterpret_cast<ulonglong2 *>(drow)[1] = make_ulonglong2(o[NG > 2 ? 2 : 0], o[NG > 3 ? 3 : 0]);
             } else {
