@@ -5,6 +5,7 @@ then the device time per kernel name.
   python tools/timeline.py                 # cfg3 16384^3 mul_strassen
   python tools/timeline.py --size 65536 --addmul --summary   # cfg5
   python tools/timeline.py --size 4096 --cutoff 1024          # cfg2
+  python tools/timeline.py --cfg4 [--addmul]                  # cfg4
 """
 import argparse
 import collections
@@ -22,6 +23,8 @@ ap.add_argument("--size", type=int, default=16384)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--addmul", action="store_true")
 ap.add_argument("--cutoff", type=int, default=0, help="0 = device default")
+ap.add_argument("--cfg4", action="store_true",
+                help="cfg4: 10000x7001 . 7001x12345 Bernoulli(0.1), mul_strassen")
 ap.add_argument("--summary", action="store_true",
                 help="only the per-kernel totals, not every launch")
 args = ap.parse_args()
@@ -29,6 +32,11 @@ n = args.size
 torch.cuda.set_device(0)
 a, b = g.random(n, n, 51 if n > 16384 else 31), g.random(n, n, 52 if n > 16384 else 32)
 c = g.random(n, n, 53) if args.addmul else None
+if args.cfg4:
+    thr = (1 << 64) // 10
+    a = g.bernoulli(10000, 7001, 41, threshold=thr)
+    b = g.bernoulli(7001, 12345, 42, threshold=thr)
+    c = g.random(10000, 12345, 43) if args.addmul else None
 
 
 params = g.MulParams(cutoff=args.cutoff, k=8) if args.cutoff else None
