@@ -369,6 +369,36 @@ def test_cfg5_addmul_digest(digests):
     assert O.digest(c0.to_numpy()) == digests["cfg5_addmul"]
 
 
+def test_max_size_engines_agree():
+    """Beyond cfg5 (the largest shapes one B200 holds comfortably, run by
+    tools/max_size.py at 131072^3): here 98304 x 81920 x 90112 with a ragged
+    twin, where the oracle cannot follow -- the tensor-core recursion and the
+    M4RM engine (independent kernels) must agree bit for bit, and the result
+    must pass Freivalds through a third path (one-word M4RM tiles)."""
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    if free < 100 << 30:
+        pytest.skip("needs ~100 GB of free HBM")
+    prev = g.get_engine()
+    try:
+        for m, l, n in ((98304, 81920, 90112), (70001, 65537, 66003)):
+            a, b = g.random(m, l, 81), g.random(l, n, 82)
+            g.set_engine("tc-f4")
+            c1 = g.mul_strassen(a, b)
+            g.release_workspace()
+            g.set_engine("m4rm")
+            c2 = g.mul_strassen(a, b)
+            g.release_workspace()
+            g.set_engine("tc-f4")
+            assert g.equal(c1, c2), (m, l, n)
+            assert g.trailing_bits_clean(c1)
+            assert _freivalds(c1, a, b)
+            del a, b, c1, c2
+    finally:
+        g.set_engine(prev)
+        g.release_workspace()
+
+
 def test_freivalds_detects_fault():
     a, b = g.random(2048, 2048, 1), g.random(2048, 2048, 2)
     c = g.mul_strassen(a, b)

@@ -57,6 +57,40 @@ def test_sharded_shards_match_full_product(nccl_group, engine):
         g.set_engine(prev)
 
 
+@pytest.mark.parametrize("pr,pc", [(2, 2), (1, 4), (4, 2)])
+def test_grid_blocks_match_full_product(nccl_group, pr, pc):
+    """Process grid pr x pc on the device, ranks emulated one at a time in
+    the world-of-one NCCL group: rank (i, j) multiplies A's rows_i by the
+    owned column block B_j (broadcast inside its column group: here the
+    group of one) and must reproduce C[rows_i, cols_j], plain and
+    accumulating, ragged right edge included."""
+    from paper_0811_1714_b200.sharded import ProcessGrid, mul_sharded_grid
+    m, l, n = 2900, 2300, 3001
+    world = pr * pc
+    params = g.MulParams(cutoff=512)
+    a_full, b_full = g.random(m, l, 17), g.random(l, n, 18)
+    c0_full = g.random(m, n, 19)
+    full = g.mul_strassen(a_full, b_full, params).to_numpy()
+    full_acc = full ^ c0_full.to_numpy()
+    for rank in range(world):
+        grid = ProcessGrid(world, rank, pr, pc)      # no groups: emulated
+        (r0, r1), (c0, c1) = grid.rows(m), grid.cols(n)
+        if r1 == r0 or c1 == c0:
+            continue
+        w0, w1 = c0 // 64, c0 // 64 + g.words_per_row(c1 - c0)
+        a_blk = g.random(r1 - r0, l, 17, row_base=r0)
+        b_blk = g.copy_out(g.window(b_full, 0, c0, l, c1 - c0))
+        # src_row=None: this rank's own rows of B_j are the source (in the
+        # world of one that is all of them; a grid-row root would name a
+        # global rank that does not exist here)
+        c_blk = mul_sharded_grid(a_blk, b_blk, grid, params, src_row=None, npanels=3)
+        assert np.array_equal(c_blk.to_numpy(), full[r0:r1, w0:w1]), (rank, "plain")
+        assert g.trailing_bits_clean(c_blk)
+        c_acc = g.copy_out(g.window(c0_full, r0, c0, r1 - r0, c1 - c0))
+        mul_sharded_grid(a_blk, b_blk, grid, params, src_row=None, npanels=2, c=c_acc)
+        assert np.array_equal(c_acc.to_numpy(), full_acc[r0:r1, w0:w1]), (rank, "acc")
+
+
 def test_sharded_cfg3_digest(nccl_group, digests):
     from paper_0811_1714_b200.sharded import mul_sharded
     a, b = g.random(16384, 16384, 31), g.random(16384, 16384, 32)
