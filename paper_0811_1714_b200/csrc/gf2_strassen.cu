@@ -50,6 +50,67 @@ constexpr unsigned swap12(unsigned m) { return (m & 9u) | ((m & 2u) << 1) | ((m 
 // product q = 7p + i lands in these quadrants of C_p (transpose of kSC)
 constexpr unsigned kSCT[7] = {0xF, 0x1, 0x2, 0x4, 0xA, 0xE, 0xC};
 
+// Tensor-core leaves when the batch is big enough to amortize the expansion
+// and each leaf is at least tensor_min_leaf() (640) on every side; smaller
+// leaves run faster on M4RM.
+bool tc_leaves(int64_t m, int64_t l, int64_t n, int depth) {
+    if (g_engine == 0) return false;
+    const int64_t lm = m >> depth, ll = l >> depth, ln = n >> depth;
+    double leaf = (double)lm * (double)ll * (double)ln;
+    for (int i = 0; i < depth; ++i) leaf *= 7.0;
+    const int64_t ml = tensor_min_leaf();
+    return leaf >= tensor_min_work() && lm >= ml && ln >= ml && ll >= ml;
+}
+
+// Workspace layout of strassen_core_tc at `depth`: which levels are
+// materialized and where (64-bit words from the workspace base).
+struct TcLayout {
+    bool fpost, bt;
+    int last, fp, lastA;
+    int64_t offA[24], offB[24], offC[24], offBt0, total;
+};
+TcLayout tc_layout(const int64_t *M, const int64_t *L, const int64_t *N, const int64_t *Lw, const int64_t *Nw,
+                   const int64_t *P, int depth) {
+    TcLayout y{};
+    // Post-additions of the last level fused into the GEMM epilogue (red.xor
+    // into C_{d-1}) unless the leaves are shallow in K: below
+    // GF2_POST_FUSE_MIN_K the leaf products are stored plainly into C_d and
+    // one more combine pass folds them up (red.xor traffic, not MMA time,
+    // bounds short-K tiles; DESIGN.md §4.5).
+    // Default: 1024-deep leaves (cfg2 at the reference's cutoff 1024) store
+    // plainly -- cfg2 63.7 -> 60.6 us, 8192^3 at cutoff 1024 310 -> 285 us --
+    // while deeper leaves (2048: even; 4096+: fused faster) and the shallow
+    // 512-cutoff leaves (736 deep: fused 1.3 us faster) keep the fused form.
+    static const int64_t post_min_k = getenv("GF2_POST_FUSE_MIN_K") ? atoll(getenv("GF2_POST_FUSE_MIN_K")) : -1;
+    y.fpost = post_min_k >= 0 ? L[depth] >= post_min_k : !(L[depth] >= 1024 && L[depth] < 2048);
+    y.last = y.fpost ? depth - 1 : depth;  // deepest materialized C level
+    // pre-addition levels fused into the expansion (GF2_FUSE_LEVELS=2 folds
+    // two levels into it; one is faster on B200, DESIGN.md §4.4)
+    static const int fuse_env = getenv("GF2_FUSE_LEVELS") ? atoi(getenv("GF2_FUSE_LEVELS")) : 1;
+    y.fp = (depth >= 2 && fuse_env >= 2) ? 2 : 1;
+    y.lastA = depth - y.fp;             // deepest materialized A/B level
+    // FP4 engine: its MMA wants B K-major, so B0 is transposed once here and
+    // the B side of the recursion runs on B^T (quadrants 12 and 21 swap)
+    y.bt = g_engine == 3;
+    int64_t total = 0;
+    for (int i = 1; i <= y.last; ++i) {
+        if (i <= y.lastA) {
+            y.offA[i] = total;
+            total += P[i] * M[i] * Lw[i];
+            y.offB[i] = total;
+            total += P[i] * L[i] * Nw[i];
+        }
+        y.offC[i] = total;
+        total += P[i] * M[i] * Nw[i];
+    }
+    // B^T of the whole operand is materialized only when no pre-addition level
+    // is (lastA == 0); otherwise level 0's B pre-addition writes transposed
+    y.offBt0 = total;
+    if (y.bt && y.lastA == 0) total += N[0] * Lw[0];
+    y.total = total;
+    return y;
+}
+
 // Tensor-core engine: levels 0..d-2 as below, and the LAST level fused into
 // the product launch -- its pre-additions into the byte expansion, its
 // post-additions into the UMMA epilogue (red.global.xor into C_{d-1}).
@@ -64,41 +125,11 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
         Nw[i] = N[i] / kWordBits;
         P[i] = i == 0 ? 1 : P[i - 1] * 7;
     }
-    // Post-additions of the last level fused into the GEMM epilogue (red.xor
-    // into C_{d-1}) unless the leaves are shallow in K: below
-    // GF2_POST_FUSE_MIN_K the leaf products are stored plainly into C_d and
-    // one more combine pass folds them up (red.xor traffic, not MMA time,
-    // bounds short-K tiles; DESIGN.md §4.5).
-    // Default: 1024-deep leaves (cfg2 at the reference's cutoff 1024) store
-    // plainly -- cfg2 63.7 -> 60.6 us, 8192^3 at cutoff 1024 310 -> 285 us --
-    // while deeper leaves (2048: even; 4096+: fused faster) and the shallow
-    // 512-cutoff leaves (736 deep: fused 1.3 us faster) keep the fused form.
-    static const int64_t post_min_k = getenv("GF2_POST_FUSE_MIN_K") ? atoll(getenv("GF2_POST_FUSE_MIN_K")) : -1;
-    const bool fpost = post_min_k >= 0 ? L[depth] >= post_min_k : !(L[depth] >= 1024 && L[depth] < 2048);
-    const int last = fpost ? depth - 1 : depth;  // deepest materialized C level
-    // pre-addition levels fused into the expansion (GF2_FUSE_LEVELS=2 folds
-    // two levels into it; one is faster on B200, DESIGN.md §4.4)
-    static const int fuse_env = getenv("GF2_FUSE_LEVELS") ? atoi(getenv("GF2_FUSE_LEVELS")) : 1;
-    const int fp = (depth >= 2 && fuse_env >= 2) ? 2 : 1;
-    const int lastA = depth - fp;             // deepest materialized A/B level
-    // FP4 engine: its MMA wants B K-major, so B0 is transposed once here and
-    // the B side of the recursion runs on B^T (quadrants 12 and 21 swap)
-    const bool bt = g_engine == 3;
-    int64_t offA[24], offB[24], offC[24], total = 0;
-    for (int i = 1; i <= last; ++i) {
-        if (i <= lastA) {
-            offA[i] = total;
-            total += P[i] * M[i] * Lw[i];
-            offB[i] = total;
-            total += P[i] * L[i] * Nw[i];
-        }
-        offC[i] = total;
-        total += P[i] * M[i] * Nw[i];
-    }
-    // B^T of the whole operand is materialized only when no pre-addition level
-    // is (lastA == 0); otherwise level 0's B pre-addition writes transposed
-    const int64_t offBt0 = total;
-    if (bt && lastA == 0) total += N[0] * Lw[0];
+    const TcLayout ly = tc_layout(M, L, N, Lw, Nw, P, depth);
+    const bool fpost = ly.fpost, bt = ly.bt;
+    const int last = ly.last, fp = ly.fp, lastA = ly.lastA;
+    const int64_t *offA = ly.offA, *offB = ly.offB, *offC = ly.offC;
+    const int64_t offBt0 = ly.offBt0, total = ly.total;
     GF2_TRY(pool_setup());
     u64 *ws = nullptr;
     if (total) {
@@ -236,17 +267,7 @@ int strassen_core_tc(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0,
 
 int strassen_core(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0, int depth, int accumulate,
                   cudaStream_t s) {
-    if (g_engine != 0) {
-        // tensor-core leaves when the batch is big enough to amortize the
-        // expansion and each leaf is at least tensor_min_leaf() (640) on every
-        // side; smaller leaves run faster on M4RM
-        const int64_t lm = A0.nrows >> depth, ll = A0.ncols >> depth, ln = B0.ncols >> depth;
-        double leaf = (double)lm * (double)ll * (double)ln;
-        for (int i = 0; i < depth; ++i) leaf *= 7.0;
-        const int64_t ml = tensor_min_leaf();
-        if (leaf >= tensor_min_work() && lm >= ml && ln >= ml && ll >= ml)
-            return strassen_core_tc(C0, A0, B0, depth, accumulate, s);
-    }
+    if (tc_leaves(A0.nrows, A0.ncols, B0.ncols, depth)) return strassen_core_tc(C0, A0, B0, depth, accumulate, s);
     int64_t M[24], L[24], N[24], Lw[24], Nw[24], P[24];
     for (int i = 0; i <= depth; ++i) {
         M[i] = A0.nrows >> i;
@@ -352,6 +373,84 @@ int strassen_core(const gf2_view &C0, const gf2_view &A0, const gf2_view &B0, in
 
 }  // namespace
 
+// Bytes of pooled workspace strassen_core asks for at `depth` on an
+// m x l x n product: the level buffers, and on a tensor engine one chunk of
+// expanded leaf operands (<= 8 GiB, launch_umma_job / launch_umma_f4).
+static double core_ws_bytes(int64_t m, int64_t l, int64_t n, int depth) {
+    int64_t M[24], L[24], N[24], Lw[24], Nw[24], P[24];
+    for (int i = 0; i <= depth; ++i) {
+        M[i] = m >> i;
+        L[i] = l >> i;
+        N[i] = n >> i;
+        Lw[i] = L[i] / kWordBits;
+        Nw[i] = N[i] / kWordBits;
+        P[i] = i == 0 ? 1 : P[i - 1] * 7;
+    }
+    if (!tc_leaves(m, l, n, depth)) {
+        double words = 0;
+        for (int i = 1; i <= depth; ++i)
+            words += (double)P[i] * ((double)M[i] * Lw[i] + (double)L[i] * Nw[i] + (double)M[i] * Nw[i]);
+        // the batched M4RM launch stages a word-major copy of every leaf's A
+        // (rows padded to 256) while it runs
+        words += (double)P[depth] * (double)Lw[depth] * (double)((M[depth] + 255) / 256 * 256);
+        return words * 8.0;
+    }
+    const TcLayout ly = tc_layout(M, L, N, Lw, Nw, P, depth);
+    double per;  // bytes of expanded operands per leaf
+    if (g_engine == 3) {
+        const double kb = (double)((L[depth] + 63) / 64 * 32), np = (double)((N[depth] + 63) / 64 * 64);
+        per = ((double)M[depth] + np) * kb;
+    } else {
+        const double kp = (double)((L[depth] + 15) / 16 * 16), np = (double)((N[depth] + 15) / 16 * 16);
+        per = (double)M[depth] * kp + (double)L[depth] * np;
+    }
+    return (double)ly.total * 8.0 + std::min((double)P[depth] * per, 8.0 * 1073741824.0);
+}
+
+// What the pool can hand out without going over the device: free memory plus
+// the blocks the pool holds but nothing uses. GF2_WS_LIMIT (bytes) replaces
+// it (tests). Negative: unknown, no limit applied.
+static double ws_budget() {
+    static const double env = getenv("GF2_WS_LIMIT") ? atof(getenv("GF2_WS_LIMIT")) : 0.0;
+    if (env > 0) return env;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+        cudaGetLastError();
+        return -1.0;
+    }
+    double idle = 0;
+    int dev = 0;
+    cudaMemPool_t pool;
+    uint64_t reserved = 0, used = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess &&
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
+        idle = (double)(reserved - used);
+    cudaGetLastError();
+    return 0.95 * ((double)free_b + idle);
+}
+
+// Deepest recursion <= depth whose workspace fits the device (HBM is
+// plentiful, so every level keeps its own buffers -- until a 131072^3
+// product on the M4RM engine asks for 146 GB). A shallower recursion is the
+// same product with larger leaves, so it is taken instead of failing with
+// out-of-memory; depth 1 is the floor (then the allocation reports OOM).
+// Only products asking for more than 4 GiB pay for the query.
+static int fit_depth(int64_t m, int64_t l, int64_t n, int depth, cudaStream_t s) {
+    static const bool forced = getenv("GF2_WS_LIMIT") != nullptr;
+    if (depth <= 1) return depth;
+    if (!forced && core_ws_bytes(m, l, n, depth) <= 4.0 * 1073741824.0) return depth;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return depth;  // no device queries inside a graph capture
+    }
+    const double budget = ws_budget();
+    if (budget < 0) return depth;
+    while (depth > 1 && core_ws_bytes(m, l, n, depth) > budget) --depth;
+    return depth;
+}
+
 // strassen.py:66-84
 void peel_split(int64_t m, int64_t l, int64_t n, int64_t cutoff, int64_t out[4]) {
     out[0] = out[1] = out[2] = out[3] = 0;
@@ -407,6 +506,14 @@ int strassen_mul(const gf2_view &C, const gf2_view &A, const gf2_view &B, int64_
     if (g_engine != 0 && cutoff < tensor_leaf_k() && (ps[1] >> ps[3]) < tensor_leaf_k()) {
         peel_split(m, l, n, tensor_leaf_k(), ps);
         if (ps[3] == 0) return m4rm_view(C, A, B, accumulate, s);
+    }
+    const int depth = fit_depth(ps[0], ps[1], ps[2], (int)ps[3], s);
+    if (depth != (int)ps[3]) {  // shallower: peel to this depth's unit
+        const int64_t unit = (int64_t)kWordBits << depth;
+        ps[0] = (m / unit) * unit;
+        ps[1] = (l / unit) * unit;
+        ps[2] = (n / unit) * unit;
+        ps[3] = depth;
     }
     const int64_t m2 = ps[0], l2 = ps[1], n2 = ps[2];
     GF2_TRY(strassen_core(sub_view(C, 0, 0, m2, n2), sub_view(A, 0, 0, m2, l2), sub_view(B, 0, 0, l2, n2),

@@ -312,6 +312,46 @@ def test_launch_and_raster_options(env, digests):
     assert lines[-1] == "True"
 
 
+@pytest.mark.parametrize("engine,n,cutoff,limit", [("m4rm", 4096, 512, 20e6), ("tc-f4", 8192, 1024, 150e6)])
+def test_workspace_limit_takes_a_shallower_recursion(engine, n, cutoff, limit):
+    """A recursion whose level buffers would not fit the device is run one or
+    more levels shallower instead of failing with out-of-memory (fit_depth in
+    csrc/gf2_strassen.cu). GF2_WS_LIMIT (bytes; read once per process, hence
+    a subprocess) stands in for a full device: the unconstrained recursions
+    here ask for 61 MiB (M4RM engine, depth 3) and 238 MiB (tc-f4, depth 2);
+    under the limit both run at depth 1, stay inside it and give the same
+    product."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import paper_0811_1714_b200 as g\n"
+        "from paper_0811_1714_b200 import _lib\n"
+        "from oracle import gf2_port as P\n"
+        "g.set_engine(%r)\n"
+        "n, cutoff = %d, %d\n"
+        "a, b = g.random(n, n, 5), g.random(n, n, 6)\n"
+        "_lib.workspace_peak(reset=True)\n"
+        "c = g.mul_strassen(a, b, g.MulParams(cutoff=cutoff, k=8))\n"
+        "print(_lib.workspace_peak())\n"
+        "P.set_threads(P.max_threads())\n"
+        "want = P.mul_strassen(P.random(n, n, 5), P.random(n, n, 6), cutoff=cutoff).words\n"
+        "print(bool((c.to_numpy() == want).all()))\n"
+    ) % (root, engine, n, cutoff)
+    peaks = {}
+    for name, env in (("free", {}), ("limited", {"GF2_WS_LIMIT": str(int(limit))})):
+        out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), cwd=root,
+                             capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        lines = out.stdout.strip().splitlines()
+        assert lines[-1] == "True", name
+        peaks[name] = int(lines[-2])
+    assert peaks["free"] > limit          # the unconstrained recursion would not have fit
+    assert peaks["limited"] <= limit
+
+
 @pytest.mark.parametrize("engine", ["m4rm", "tc-f4"])
 def test_deep_recursion_many_leaves(engine):
     """Fuzzer regression: cutoff 64 on 4546x12000x12000 recurses to depth 6

@@ -5,6 +5,9 @@ C.X == A.(B.X) (a third kernel path: one-word M4RM tiles). Also reports the
 time per multiply and the workspace high-water mark.
 
   python tools/max_size.py [OUT.json]            # 131072^3 and a ragged giant
+  python tools/max_size.py OUT.json --huge       # also 262144^3 (8 GiB per matrix):
+                                                 # the recursion is taken shallower
+                                                 # so its workspace fits the device
 """
 import json
 import sys
@@ -19,6 +22,15 @@ from paper_0811_1714_b200 import _lib  # noqa: E402
 torch.cuda.set_device(0)
 CASES = [("square 131072^3", 131072, 131072, 131072, False),
          ("ragged 100003 x 90001 x 120007, addmul", 100003, 90001, 120007, True)]
+
+
+if "--only-huge" in sys.argv:
+    sys.argv[sys.argv.index("--only-huge")] = "--huge"
+    CASES.clear()
+if "--huge" in sys.argv:
+    sys.argv.remove("--huge")
+    CASES.append(("square 262144^3 (depth limited by the workspace budget)",
+                  262144, 262144, 262144, False))
 
 
 def freivalds(c, a, b, c0=None, reps=2):
@@ -37,7 +49,8 @@ def run(engine, a, b, c0):
     g.set_engine(engine)
     _lib.workspace_peak(reset=True)
     best = None
-    for _ in range(2):
+    for _ in range(2 if a.nrows < 200000 else 1):
+        c = None
         c = g.copy_out(c0) if c0 is not None else None
         torch.cuda.synchronize()
         t0 = time.perf_counter()
