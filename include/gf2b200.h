@@ -69,8 +69,13 @@ const char *gf2_last_error(void);
  * not its width in words (a window, or a padded pitch) travels through a
  * contiguous staging buffer and is unpacked with an edge-preserving copy,
  * so no word outside B's window is written on any rank.
+ * Process grid pr x pc (sharded.py ProcessGrid / mul_sharded_grid): rank
+ * (i, j) calls this with the communicator of its COLUMN group (the pr ranks
+ * sharing column block j), c_shard = C[rows_i, cols_j], a_shard = A[rows_i, :]
+ * and b = the l x n_j column block B_j; nothing else changes, and K is never
+ * split across ranks, so there is still no reduction.
  * The Python package offers the same over torch.distributed
- * (paper_0811_1714_b200.sharded.mul_sharded). */
+ * (paper_0811_1714_b200.sharded.mul_sharded, mul_sharded_grid). */
 int gf2_mul_sharded(const gf2_view *c_shard, const gf2_view *a_shard, const gf2_view *b, void *nccl_comm,
                     int src, int npanels, int64_t cutoff, int accumulate, void *stream);
 
