@@ -42,6 +42,38 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
     return x;
 }
 
+// The same butterfly with its per-lane constants hoisted: keep[i] = the bits a
+// lane keeps at stage i, rot[i] = the left-rotation that moves the received
+// half into place (32 - sh on upper lanes: a right shift, the moved half's
+// complement is zero). 4 instructions per stage (LOP3, SHFL, SHF, LOP3)
+// instead of the selects of transpose32. MSB-first words need no bit
+// reversal around it when lane l holds row 31 - l: its result is then the
+// MSB-first word of column 31 - l (reversing bit and lane order together maps
+// the network onto itself).
+struct Bfly32 {
+    uint32_t keep[5], rot[5];
+};
+__device__ __forceinline__ Bfly32 bfly32_init(int lane) {
+    const uint32_t masks[5] = {0xFFFF0000u, 0xFF00FF00u, 0xF0F0F0F0u, 0xCCCCCCCCu, 0xAAAAAAAAu};
+    Bfly32 c;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const int sh = 16 >> i;
+        const bool up = lane & sh;
+        c.keep[i] = up ? masks[i] : ~masks[i];
+        c.rot[i] = up ? 32 - sh : sh;
+    }
+    return c;
+}
+__device__ __forceinline__ uint32_t transpose32m(uint32_t x, const Bfly32 &c) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const uint32_t got = __shfl_xor_sync(0xffffffffu, x & ~c.keep[i], 16 >> i);
+        x = (x & c.keep[i]) | __funnelshift_l(got, got, c.rot[i]);
+    }
+    return x;
+}
+
 // Per-device one-time setup: function attributes (the dynamic shared-memory
 // opt-in) belong to the device context, so "done" is tracked per device.
 // Returns true the first time it is called for `flags` on the current device.

@@ -37,17 +37,22 @@ __global__ void __launch_bounds__(256) k_transpose(const u64 *__restrict__ in, i
         tile[rr][ww] = x;
     }
     __syncthreads();
-    // units: (word column, 64-row group); bits of rows beyond `rows` are zero
-#pragma unroll 1
-    for (int u = warp; u < TR_WORDS * TR_OUT_WORDS; u += 8) {
+    // units: (word column, 64-row group); bits of rows beyond `rows` are zero.
+    // Lane l takes rows 31 - l and 63 - l of the block and ends up with
+    // columns 31 - l and 63 - l (transpose32m: MSB-first, no bit reversal).
+    const Bfly32 bf = bfly32_init(lane);
+    const int rl = 31 - lane;
+#pragma unroll 2
+    for (int it = 0; it < TR_WORDS * TR_OUT_WORDS / 8; ++it) {
+        const int u = warp + 8 * it;
         const int ww = u % TR_WORDS, g = u / TR_WORDS;
-        const u64 x0 = tile[64 * g + lane][ww], x1 = tile[64 * g + 32 + lane][ww];
-        const uint32_t c0a = transpose32(__brev((uint32_t)(x0 >> 32)), lane);
-        const uint32_t c0b = transpose32(__brev((uint32_t)(x1 >> 32)), lane);
-        const uint32_t c1a = transpose32(__brev((uint32_t)x0), lane);
-        const uint32_t c1b = transpose32(__brev((uint32_t)x1), lane);
-        stg[64 * ww + lane][g] = __brevll(((u64)c0b << 32) | c0a);  // MSB-first: row i at bit 63 - i
-        stg[64 * ww + 32 + lane][g] = __brevll(((u64)c1b << 32) | c1a);
+        const u64 x0 = tile[64 * g + rl][ww], x1 = tile[64 * g + 32 + rl][ww];
+        const uint32_t tp = transpose32m((uint32_t)(x0 >> 32), bf);  // rows 0..31, columns 0..31
+        const uint32_t tr = transpose32m((uint32_t)(x1 >> 32), bf);  // rows 32..63, columns 0..31
+        const uint32_t tq = transpose32m((uint32_t)x0, bf);          // rows 0..31, columns 32..63
+        const uint32_t ts = transpose32m((uint32_t)x1, bf);          // rows 32..63, columns 32..63
+        stg[64 * ww + rl][g] = ((u64)tp << 32) | tr;
+        stg[64 * ww + 32 + rl][g] = ((u64)tq << 32) | ts;
     }
     __syncthreads();
     const int64_t ow0 = r0 / 64;
