@@ -15,21 +15,19 @@ namespace {
 
 // out[c][r] = in[r][c]. A block stages 512 input rows x 4 words (one 32-byte
 // sector per row) in shared memory; each warp transposes 64 x 64 blocks with
-// four warp-wide 32 x 32 butterflies (transpose32m) into a shared output tile
+// four warp-wide 32 x 32 butterflies (transpose32) into a shared output tile
 // (256 rows x 8 words), written back as 16-byte stores, 64 contiguous bytes
-// per output row. Both tiles are XOR-swizzled instead of padded, so all four
-// access patterns (row-major fill, column reads by 32 consecutive rows,
-// column writes, 16-byte row reads) are bank-conflict free: with the padded
-// pitches 5 and 9, ncu counted 10.6 M conflict wavefronts in 48.8 M on a
-// kernel bound by the L1/shared data pipe.
+// per output row. The kernel is bound by the L1/shared data pipe (ncu: 87 %,
+// 21 M shuffle + 27 M shared wavefronts at 65536^2, 10.6 M of them bank
+// conflicts of the padded pitches 5 and 9). XOR-swizzled tiles without
+// padding (conflict-free on paper for all four access patterns) measured
+// slower, 447 vs 392 us at 65536^2, and were not kept.
 constexpr int TR_ROWS = 512, TR_WORDS = 4, TR_OUT_WORDS = TR_ROWS / 64;
-__device__ __forceinline__ int tr_in_col(int r, int w) { return w ^ ((r >> 2) & 3); }
-__device__ __forceinline__ int tr_out_col(int r, int g) { return g ^ ((r >> 1) & 7); }
 __global__ void __launch_bounds__(256) k_transpose(const u64 *__restrict__ in, int64_t pin, u64 *__restrict__ out,
                                                    int64_t pout, int64_t rows, int64_t cols) {
     pdl_begin();
-    __shared__ __align__(16) u64 tile[TR_ROWS][TR_WORDS];
-    __shared__ __align__(16) u64 stg[64 * TR_WORDS][TR_OUT_WORDS];
+    __shared__ u64 tile[TR_ROWS][TR_WORDS + 1];
+    __shared__ u64 stg[64 * TR_WORDS][TR_OUT_WORDS + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t wcols = words_per_row(cols), wrows = words_per_row(rows);
     const int64_t w0 = (int64_t)blockIdx.x * TR_WORDS, r0 = (int64_t)blockIdx.y * TR_ROWS;
@@ -40,7 +38,7 @@ __global__ void __launch_bounds__(256) k_transpose(const u64 *__restrict__ in, i
         const int64_t r = r0 + rr, w = w0 + ww;
         u64 x = 0;
         if (r < rows && w < wcols) x = in[r * pin + w] & (w == wcols - 1 ? tail_mask(cols) : ~0ULL);
-        tile[rr][tr_in_col(rr, ww)] = x;
+        tile[rr][ww] = x;
     }
     __syncthreads();
     // units: (word column, 64-row group); bits of rows beyond `rows` are zero.
@@ -52,15 +50,13 @@ __global__ void __launch_bounds__(256) k_transpose(const u64 *__restrict__ in, i
     for (int it = 0; it < TR_WORDS * TR_OUT_WORDS / 8; ++it) {
         const int u = warp + 8 * it;
         const int ww = u % TR_WORDS, g = u / TR_WORDS;
-        const int ra = 64 * g + rl, rb = ra + 32;
-        const u64 x0 = tile[ra][tr_in_col(ra, ww)], x1 = tile[rb][tr_in_col(rb, ww)];
+        const u64 x0 = tile[64 * g + rl][ww], x1 = tile[64 * g + 32 + rl][ww];
         const uint32_t tp = transpose32m((uint32_t)(x0 >> 32), bf);  // rows 0..31, columns 0..31
         const uint32_t tr = transpose32m((uint32_t)(x1 >> 32), bf);  // rows 32..63, columns 0..31
         const uint32_t tq = transpose32m((uint32_t)x0, bf);          // rows 0..31, columns 32..63
         const uint32_t ts = transpose32m((uint32_t)x1, bf);          // rows 32..63, columns 32..63
-        const int oa = 64 * ww + rl, ob = oa + 32;
-        stg[oa][tr_out_col(oa, g)] = ((u64)tp << 32) | tr;
-        stg[ob][tr_out_col(ob, g)] = ((u64)tq << 32) | ts;
+        stg[64 * ww + rl][g] = ((u64)tp << 32) | tr;
+        stg[64 * ww + 32 + rl][g] = ((u64)tq << 32) | ts;
     }
     __syncthreads();
     const int64_t ow0 = r0 / 64;
@@ -72,16 +68,11 @@ __global__ void __launch_bounds__(256) k_transpose(const u64 *__restrict__ in, i
         const int64_t oc = w0 * 64 + orow, ow = ow0 + 2 * ch;
         if (oc >= cols || ow >= wrows) continue;
         u64 *d = out + oc * pout + ow;
-        // logical words 2ch, 2ch + 1 share one aligned 16-byte pair under the
-        // swizzle (swapped inside it when the row's key is odd)
-        const int pc = tr_out_col(orow, 2 * ch);
-        const ulonglong2 pr = *reinterpret_cast<const ulonglong2 *>(&stg[orow][pc & ~1]);
-        const u64 v0 = (pc & 1) ? pr.y : pr.x, v1 = (pc & 1) ? pr.x : pr.y;
         if (vec && ow + 1 < wrows) {
-            *reinterpret_cast<ulonglong2 *>(d) = make_ulonglong2(v0, v1);
+            *reinterpret_cast<ulonglong2 *>(d) = make_ulonglong2(stg[orow][2 * ch], stg[orow][2 * ch + 1]);
         } else {
-            d[0] = v0;
-            if (ow + 1 < wrows) d[1] = v1;
+            d[0] = stg[orow][2 * ch];
+            if (ow + 1 < wrows) d[1] = stg[orow][2 * ch + 1];
         }
     }
 }
