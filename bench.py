@@ -75,6 +75,11 @@ def parse(argv=None):
     p.add_argument("--cutoff", type=int, default=0,
                    help="Strassen cutoff (0 = device default)")
     p.add_argument("--npanels", type=int, default=2)
+    p.add_argument("--grid", default="rows",
+                   help="N > 1 layout: 'rows' (north_star (e): C and A row-sharded, B "
+                        "broadcast to every rank), 'PRxPC' or 'auto' (process grid: "
+                        "rank (i, j) owns C[rows_i, cols_j], B's column block j is "
+                        "broadcast inside column group j)")
     p.add_argument("--sharded", action="store_true",
                    help="run the multi-GPU (NCCL) step and e2e path even at "
                         "N = 1 (a world of one; for testing it on one GPU)")
@@ -419,6 +424,7 @@ class Ctx:
         self.args, self.g, self.dev = args, g, dev
         self.world, self.rank, self.local = world, rank, local
         self.dist_on, self.flush, self.stream = dist_on, flush, stream
+        self.grid = None            # ProcessGrid when --grid is not 'rows'
 
     def max_over_ranks(self, ms: float, ok: bool = True):
         if not self.dist_on:
@@ -449,6 +455,26 @@ def digest_rows(ctx, out, w):
     from paper_0811_1714_b200.sharded import shard_rows
     width = g.words_per_row(w["n"])
     cuda_p2p = dist.get_backend() == "nccl"  # gloo (GF2_BENCH_SHARE_GPU) sends host tensors
+    if ctx.grid is not None:
+        # blocks, not row shards: rank 0 assembles the matrix on the host
+        import numpy as np
+        grid = ctx.grid
+        full = np.zeros((w["m"], width), dtype="<u8") if ctx.rank == 0 else None
+        for r in range(ctx.world):
+            r0, r1, c0, c1 = grid.block_of(r, w["m"], w["n"])
+            bw = g.words_per_row(c1 - c0)
+            if r1 == r0 or bw == 0:
+                continue
+            if r == ctx.rank == 0:
+                full[r0:r1, c0 // 64:c0 // 64 + bw] = out.to_numpy()
+            elif r == ctx.rank:
+                t = out.storage[:, :bw].contiguous()
+                dist.send(t if cuda_p2p else t.cpu(), dst=0)
+            elif ctx.rank == 0:
+                t = torch.empty((r1 - r0, bw), dtype=torch.int64, device=ctx.dev if cuda_p2p else "cpu")
+                dist.recv(t, src=r)
+                full[r0:r1, c0 // 64:c0 // 64 + bw] = t.cpu().numpy().view(np.uint64)
+        return hashlib.sha256(full.tobytes()).hexdigest() if ctx.rank == 0 else None
     h = hashlib.sha256() if ctx.rank == 0 else None
     for r in range(ctx.world):
         r0, r1 = shard_rows(w["m"], ctx.world, r)
@@ -682,6 +708,89 @@ def e2e_sharded(ctx, w, params, a, r0, r1, c0_fill, want_rank):
     return piped, serial
 
 
+def e2e_grid(ctx, w, params, a, block, c0_fill, want_rank):
+    """End to end on the process grid, one product at a time: rank (i, j)
+    uploads 1/pc of A's rows_i (the rest arrives inside its row group,
+    gather_rows), its share of column block B_j's rows (owned_rows over the
+    pr ranks of column group j) and, for addmul, its block of C0, all from
+    pinned host memory; mul_sharded_grid(src_row=None) broadcasts B_j's
+    pieces inside the column group while the panels multiply; the rank
+    downloads its block of C. Max over ranks; bytes are whole-job totals."""
+    import numpy as np
+    import torch
+    g, grid = ctx.g, ctx.grid
+    from paper_0811_1714_b200.sharded import gather_rows, mul_sharded_grid, owned_rows, shard_rows
+    m, l, n = w["m"], w["l"], w["n"]
+    r0, r1, c0, c1 = block
+    mr, nc = r1 - r0, c1 - c0
+    addmul = w["kind"] == "addmul"
+    wa, wbj = g.words_per_row(l), g.words_per_row(nc)
+    keep = []
+    # A_i: this rank uploads piece j of its rows, 64-row aligned
+    pieces = [shard_rows(mr, grid.pc, j) for j in range(grid.pc)]
+    p0, p1 = pieces[grid.j]
+    ta, hav = _pinned(p1 - p0, wa)
+    keep.append(ta)
+    g.window(a, p0, 0, p1 - p0, l).to_numpy(out=hav)
+    # B_j: this rank's rows of the column block
+    mine = owned_rows(l, grid.pr, grid.i, None)
+    tb, hbv = _pinned(l, wbj)
+    keep.append(tb)
+    full_b = g.random(l, n, w["seed_b"], device=ctx.dev)
+    for k0, k1 in mine:
+        g.window(full_b, k0, c0, k1 - k0, nc).to_numpy(out=hbv[k0:k1])
+    del full_b
+    tc, hcv = _pinned(mr, wbj)
+    keep.append(tc)
+    hc0v = None
+    if addmul:
+        t, hc0v = _pinned(mr, wbj)
+        keep.append(t)
+        c0_fill().to_numpy(out=hc0v)
+    ad, bd, cd = g.create(mr, l, ctx.dev), g.create(l, nc, ctx.dev), g.create(mr, nc, ctx.dev)
+    roots = grid.row_ranks(grid.i)
+
+    def e2e_step():
+        if p1 > p0:
+            g.from_numpy(hav, l, out=g.window(ad, p0, 0, p1 - p0, l), nonblocking=True)
+        if grid.pc > 1:
+            gather_rows(ad.storage, pieces, roots, group=grid.row_group)
+        for k0, k1 in mine:
+            g.from_numpy(hbv[k0:k1], nc, out=g.window(bd, k0, 0, k1 - k0, nc), nonblocking=True)
+        if addmul:
+            g.from_numpy(hc0v, nc, out=cd, nonblocking=True)
+        mul_sharded_grid(ad, bd, grid, params, src_row=None, npanels=ctx.args.npanels, c=cd,
+                         accumulate=addmul)
+        g.core._download(cd, hcv, nonblocking=True)
+
+    for _ in range(max(1, ctx.args.warmup)):
+        e2e_step()
+    ctx.barrier()
+    ee = []
+    for _ in range(ctx.args.steps):
+        ctx.flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(ctx.stream)
+        e2e_step()
+        e1.record(ctx.stream)
+        ee.append((e0, e1))
+    torch.cuda.synchronize()
+    ms, ok = ctx.max_over_ranks(sum(x.elapsed_time(y) for x, y in ee) / ctx.args.steps,
+                                bool(np.array_equal(hcv, want_rank)))
+    del ad, bd, cd, keep
+    return {"unit": UNIT, "value": m * l * n / (ms * 1e-3), "ms_per_step": ms,
+            "verified_vs_device_result": ok,
+            "h2d_bytes_per_step": int(m * wa * 8 + l * g.words_per_row(n) * 8
+                                      + (m * g.words_per_row(n) * 8 if addmul else 0)),
+            "d2h_bytes_per_step": int(m * g.words_per_row(n) * 8),
+            "mode": f"process grid {grid.pr}x{grid.pc}, one product at a time: each rank uploads "
+                    "1/pc of A's rows_i (gathered inside the row group), its rows of column "
+                    "block B_j" + (", its block of C0" if addmul else "") + " from pinned host "
+                    "memory, mul_sharded_grid(src_row=None) broadcasts B_j's pieces inside the "
+                    "column group while panels multiply, and downloads its block of C; max over ranks"}
+
+
 def roofline_for(ctx, kern_ms, kern_ops, kern_n, steps, total_ms):
     """Roofline of the dominant kernel (the batched leaf-product launch),
     achieved from its live CUDA-event time inside the timed region."""
@@ -749,24 +858,45 @@ def measure(ctx, w, primary: bool):
     import torch
     g, args = ctx.g, ctx.args
     from paper_0811_1714_b200 import _lib
-    from paper_0811_1714_b200.sharded import mul_sharded, shard_rows
+    from paper_0811_1714_b200.sharded import mul_sharded, mul_sharded_grid, shard_rows
 
     m, l, n = w["m"], w["l"], w["n"]
     addmul = w["kind"] == "addmul"
     params = g.default_params() if not args.cutoff else \
         g.MulParams(cutoff=args.cutoff, k=8)
-    r0, r1 = shard_rows(m, ctx.world, ctx.rank) if ctx.dist_on else (0, m)
+    grid = ctx.grid
+    if grid is not None:
+        (r0, r1), (c0, c1) = grid.rows(m), grid.cols(n)
+    else:
+        r0, r1 = shard_rows(m, ctx.world, ctx.rank) if ctx.dist_on else (0, m)
+        c0, c1 = 0, n
     a = g.random(r1 - r0, l, w["seed_a"], device=ctx.dev, row_base=r0)
-    b = g.random(l, n, w["seed_b"], device=ctx.dev) if (ctx.world == 1 or ctx.rank == 0) \
-        else g.create(l, n, device=ctx.dev)
-    c = g.create(r1 - r0, n, device=ctx.dev) if addmul else None
+    c_rows = None
+    if grid is not None:
+        # column block B_j: an owned l x n_j matrix, filled on grid row 0 (the
+        # seeded generator indexes whole rows, so the block is cut from B)
+        b = g.create(l, c1 - c0, device=ctx.dev)
+        if grid.i == 0:
+            g.copy_into(b, g.window(g.random(l, n, w["seed_b"], device=ctx.dev), 0, c0, l, c1 - c0))
+        c = g.create(r1 - r0, c1 - c0, device=ctx.dev) if addmul else None
+        c_rows = g.create(r1 - r0, n, device=ctx.dev) if addmul else None
+    else:
+        b = g.random(l, n, w["seed_b"], device=ctx.dev) if (ctx.world == 1 or ctx.rank == 0) \
+            else g.create(l, n, device=ctx.dev)
+        c = g.create(r1 - r0, n, device=ctx.dev) if addmul else None
 
     def reset():
-        if addmul:
+        if addmul and grid is not None:
+            g.random_into(c_rows, w["seed_c"], row_base=r0)
+            g.copy_into(c, g.window(c_rows, 0, c0, r1 - r0, c1 - c0))
+        elif addmul:
             g.random_into(c, w["seed_c"], row_base=r0)
         return c
 
     def step():
+        if grid is not None:
+            return mul_sharded_grid(a, b, grid, params, src_row=0, npanels=args.npanels,
+                                    c=c if addmul else None, accumulate=True)
         if not ctx.dist_on:
             if addmul:
                 g.addmul(c, a, b, params)
@@ -825,7 +955,12 @@ def measure(ctx, w, primary: bool):
 
     res["e2e"] = res["e2e_serial"] = None
     if not args.no_e2e:
-        if ctx.dist_on:
+        if grid is not None:
+            want_rank = out.to_numpy()
+            out = None
+            res["e2e"] = res["e2e_serial"] = e2e_grid(
+                ctx, w, params, a, (r0, r1, c0, c1), reset, want_rank)
+        elif ctx.dist_on:
             want_rank = out.to_numpy()
             out = None
             res["e2e"], res["e2e_serial"] = e2e_sharded(
@@ -839,7 +974,7 @@ def measure(ctx, w, primary: bool):
                 e = res[k]
                 ok = e.get("verified_sha256", e.get("verified_vs_device_result"))
                 res["verified_sha256"] = res["verified_sha256"] and bool(ok)
-    del a, b, c, out
+    del a, b, c, c_rows, out
 
     res["roofline"] = roofline_for(ctx, kern_ms, kern_ops, kern_n, args.steps, total_ms) \
         if ctx.rank == 0 else None
@@ -874,7 +1009,9 @@ def _line_part(ctx, res):
                    "m": m, "l": l, "n": n, "cutoff": params.cutoff,
                    "seeds": [w["seed_a"], w["seed_b"]] + ([w["seed_c"]] if "seed_c" in w else []),
                    "parallelism": "single" if not ctx.dist_on else
-                   f"rows{ctx.world} + NCCL broadcast of B ({args.npanels} panels)",
+                   (f"grid{ctx.grid.pr}x{ctx.grid.pc} + NCCL broadcast of B's column blocks "
+                    f"inside column groups ({args.npanels} panels)" if ctx.grid is not None else
+                    f"rows{ctx.world} + NCCL broadcast of B ({args.npanels} panels)"),
                    "l2": "flushed between timed steps (512 MiB write)"
                          + ("; C refilled with C0 before each step, outside the "
                             "timed events" if w["kind"] == "addmul" else "")},
@@ -935,6 +1072,19 @@ def run_b200(args):
     w = dict(WORKLOADS[args.workload])
     if args.size:
         w.update(m=args.size, l=args.size, n=args.size)
+    if dist_on and world > 1 and args.grid != "rows":
+        from paper_0811_1714_b200.sharded import ProcessGrid, choose_grid
+        if args.grid == "auto":
+            pr, pc = choose_grid(world, w["m"], w["n"])
+        else:
+            try:
+                pr, pc = (int(x) for x in args.grid.lower().split("x"))
+            except ValueError:
+                die(f"--grid {args.grid!r}: expected rows, auto or PRxPC")
+        if pr * pc != world:
+            die(f"--grid {pr}x{pc} does not cover {world} ranks")
+        if pc > 1:                      # PR x 1 is the row-sharded layout
+            ctx.grid = ProcessGrid(world, rank, pr, pc, make_groups=True)
     main_res = measure(ctx, w, primary=True)
     extra = {}
     if not args.size:

@@ -54,15 +54,19 @@ def shard_cols(n: int, parts: int, j: int, align: int = 2 * _WORD):
 
 
 def choose_grid(world: int, m: int, n: int) -> tuple[int, int]:
-    """pr x pc = world with the squarest C blocks (m/pr against n/pc); ties
-    go to more row blocks, so 2 ranks keep the row-sharded layout."""
+    """pr x pc = world with the squarest C blocks (m/pr against n/pc). Two
+    ranks keep the row-sharded layout; from 4 ranks on a tie goes to more
+    COLUMN blocks: a rank then receives and expands less of B (the dearer
+    side: it is transposed on the way), measured on one B200 at N = 8 as
+    8.6 ms per cfg5 block on 2 x 4 against 10.1 ms on 4 x 2
+    (profiles/r02_grid_rank_compute.txt)."""
     best = None
     for pr in range(1, world + 1):
         if world % pr:
             continue
         pc = world // pr
         h, w = -(-m // pr), -(-n // pc)
-        key = (max(h, w) / max(1, min(h, w)), pc)
+        key = (max(h, w) / max(1, min(h, w)), pc if world <= 2 else -pc)
         if best is None or key < best[0]:
             best = (key, (pr, pc))
     return best[1]

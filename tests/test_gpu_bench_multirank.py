@@ -34,3 +34,26 @@ def test_bench_two_ranks_share_one_gpu():
     assert "share_gpu_test" in d
     assert d["e2e"]["verified_vs_device_result"] is True
     assert d["config"]["parallelism"].startswith("rows2")
+
+
+def test_bench_process_grid_share_one_gpu():
+    """`--gpus 4 --grid 2x2` the same way: rank (i, j) owns C[rows_i, cols_j],
+    B's column blocks are cut on grid row 0 and broadcast inside the column
+    groups, rank 0 assembles the blocks and checks the cfg3 digest; the
+    grid's end-to-end step (A_i gathered inside row groups, B_j's rows
+    distributed over the column group) must reproduce the device result."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, GF2_BENCH_SHARE_GPU="1")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--grid", "2x2",
+                          "--steps", "2", "--warmup", "1", "--extra", "none", "--no-cpu-baseline"],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 4 and d["verified_sha256"] is True
+    assert d["e2e"]["verified_vs_device_result"] is True
+    assert d["config"]["parallelism"].startswith("grid2x2")

@@ -176,7 +176,7 @@ def test_grid_partition_properties():
             if cover is not None:
                 assert (cover == 1).all()
     assert choose_grid(2, 16384, 16384) == (2, 1)      # ties keep row sharding
-    assert choose_grid(8, 65536, 65536) == (4, 2)
+    assert choose_grid(8, 65536, 65536) == (2, 4)      # ties from 4 ranks on: more column blocks
     with pytest.raises(ValueError):
         ProcessGrid(4, 0, 3, 2)
     assert shard_cols(300, 2, 0) == (0, 256) and shard_cols(300, 2, 1) == (256, 300)
