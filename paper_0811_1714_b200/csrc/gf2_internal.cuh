@@ -27,29 +27,14 @@ __host__ __device__ inline u64 tail_mask(int64_t ncols) {
 
 // 32 x 32 bit transpose across a warp: lane L bit P <-> lane P bit L
 // (5 butterfly stages; at stage s the lanes swap the bits whose lane and
-// position s-bits differ).
-__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
-    const uint32_t masks[5] = {0xFFFF0000u, 0xFF00FF00u, 0xF0F0F0F0u, 0xCCCCCCCCu, 0xAAAAAAAAu};
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-        const int sh = 16 >> i;
-        const uint32_t m = masks[i];
-        const bool up = lane & sh;
-        const uint32_t give = up ? (x & ~m) : (x & m);
-        const uint32_t got = __shfl_xor_sync(0xffffffffu, give, sh);
-        x = up ? ((x & m) | (got >> sh)) : ((x & ~m) | (got << sh));
-    }
-    return x;
-}
-
-// The same butterfly with its per-lane constants hoisted: keep[i] = the bits a
-// lane keeps at stage i, rot[i] = the left-rotation that moves the received
-// half into place (32 - sh on upper lanes: a right shift, the moved half's
-// complement is zero). 4 instructions per stage (LOP3, SHFL, SHF, LOP3)
-// instead of the selects of transpose32. MSB-first words need no bit
-// reversal around it when lane l holds row 31 - l: its result is then the
-// MSB-first word of column 31 - l (reversing bit and lane order together maps
-// the network onto itself).
+// position s-bits differ). The per-lane constants are hoisted: keep[i] = the
+// bits a lane keeps at stage i, rot[i] = the left-rotation that moves the
+// received half into place (32 - sh on upper lanes: a right shift, the moved
+// half's complement is zero) -- 4 instructions per stage (LOP3, SHFL, SHF,
+// LOP3). MSB-first words need no bit reversal around it: with lane l holding
+// row 31 - l, the result is the MSB-first word of column 31 - l (reversing
+// bit and lane order together maps the network onto itself); with lane l
+// holding row l, it is column 31 - l with the rows LSB-first.
 struct Bfly32 {
     uint32_t keep[5], rot[5];
 };

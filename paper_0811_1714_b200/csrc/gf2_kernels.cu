@@ -249,20 +249,24 @@ __global__ void __launch_bounds__(256) k_combine_t(CombineArgs p) {
     // writes (ncu: 32 sectors per 16-byte store request, each written twice)
     const bool vec32 = vec && (p.dst_pitch % 4 == 0) && (p.dst_stride % 4 == 0) &&
                        ((uintptr_t)db % 32 == 0);
+    // transpose32m: lane l takes rows 31 - l and 63 - l of a 64-row group and
+    // ends up with column 31 - l (half 0) or 63 - l (half 1), MSB-first, with
+    // no bit reversals
+    const Bfly32 bf = bfly32_init(lane);
+    const int rl = 31 - lane;
 #pragma unroll 1
     for (int half = 0; half < 2; ++half) {
-        u64 T[4][NG];  // [quadrant][64-row group]: transposed word of row 64w + 32 half + lane
+        u64 T[4][NG];  // [quadrant][64-row group]: transposed word of row 64w + 32 half + 31 - lane
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd)
 #pragma unroll
             for (int g = 0; g < NG; ++g) {
-                const u64 x0 = tile[qd][64 * g + lane][warp], x1 = tile[qd][64 * g + 32 + lane][warp];
+                const u64 x0 = tile[qd][64 * g + rl][warp], x1 = tile[qd][64 * g + 32 + rl][warp];
                 const uint32_t p0 = half ? (uint32_t)x0 : (uint32_t)(x0 >> 32);
                 const uint32_t p1 = half ? (uint32_t)x1 : (uint32_t)(x1 >> 32);
-                const uint32_t a = transpose32(__brev(p0), lane), b = transpose32(__brev(p1), lane);
-                T[qd][g] = __brevll(((u64)b << 32) | a);
+                T[qd][g] = ((u64)transpose32m(p0, bf) << 32) | transpose32m(p1, bf);
             }
-        const int64_t orow = w * 64 + half * 32 + lane;  // output row (< 64 W, always in range)
+        const int64_t orow = w * 64 + half * 32 + rl;  // output row (< 64 W, always in range)
 #pragma unroll
         for (int q = 0; q < 7; ++q) {
             u64 o[NG];

@@ -204,19 +204,24 @@ __global__ void __launch_bounds__(256) k_expand4_cols(ExpandArgs a) {
     }
     __syncthreads();
     const int64_t kbytes = a.dp;  // bytes per output row
+    const Bfly32 bf = bfly32_init(lane);
 #pragma unroll 1
     for (int u = 0; u < F4T_WORDS / 8; ++u) {
         const int ww = warp * (F4T_WORDS / 8) + u;
         const int64_t w = w0 + ww;
         if (w >= width) break;
-        u64 ca[4], cb[4];  // column lane / lane + 32, K block kb (64 entries each)
+        // column 31 - lane / 63 - lane, K block kb (64 entries each, bit i =
+        // entry i): the butterfly on the raw MSB-first halves, lane l holding
+        // row l, leaves lane l with column 31 - l and rows LSB-first -- the
+        // K-vector the nibble expansion wants, with no bit reversal
+        u64 ca[4], cb[4];
 #pragma unroll
         for (int kb = 0; kb < 4; ++kb) {
             const u64 x0 = tile[kb * 64 + lane][ww], x1 = tile[kb * 64 + 32 + lane][ww];
-            const uint32_t c0a = transpose32(__brev((uint32_t)(x0 >> 32)), lane);
-            const uint32_t c0b = transpose32(__brev((uint32_t)(x1 >> 32)), lane);
-            const uint32_t c1a = transpose32(__brev((uint32_t)x0), lane);
-            const uint32_t c1b = transpose32(__brev((uint32_t)x1), lane);
+            const uint32_t c0a = transpose32m((uint32_t)(x0 >> 32), bf);
+            const uint32_t c0b = transpose32m((uint32_t)(x1 >> 32), bf);
+            const uint32_t c1a = transpose32m((uint32_t)x0, bf);
+            const uint32_t c1b = transpose32m((uint32_t)x1, bf);
             ca[kb] = ((u64)c0b << 32) | c0a;
             cb[kb] = ((u64)c1b << 32) | c1a;
         }
@@ -230,7 +235,7 @@ __global__ void __launch_bounds__(256) k_expand4_cols(ExpandArgs a) {
 #pragma unroll
             for (int kb = 0; kb < 4; ++kb) {
                 const u64 v = half ? cb[kb] : ca[kb];
-                uint4 *o = reinterpret_cast<uint4 *>(stg + lane * F4T_STG_PITCH + 32 * kb);
+                uint4 *o = reinterpret_cast<uint4 *>(stg + (31 - lane) * F4T_STG_PITCH + 32 * kb);
                 o[0] = make_uint4(nib_word(v, 0), nib_word(v, 1), nib_word(v, 2), nib_word(v, 3));
                 o[1] = make_uint4(nib_word(v, 4), nib_word(v, 5), nib_word(v, 6), nib_word(v, 7));
             }
