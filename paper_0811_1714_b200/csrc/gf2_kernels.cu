@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(256, 3) k_combine_all(CombineArgs p, int64_t w
 // Level-0 B pre-addition fused with the transpose the FP4 engine needs:
 // dst_q = (XOR_{i in mask[q]} quadrant_i(src))^T, q < 7. A block stages the
 // 4 quadrants' tiles (256 rows x 8 words each) in shared memory; warp w
-// transposes word column w of every quadrant (transpose32, linear, so the
+// transposes word column w of every quadrant (transpose32m, linear, so the
 // XOR commutes with it) and writes each transposed row's 4 words with two
 // 16-byte stores.
 // CT_ROWS = 256 (4 groups of 64 rows, 16-byte output stores); 64-row tiles

@@ -15,7 +15,7 @@ namespace {
 
 // out[c][r] = in[r][c]. A block stages 512 input rows x 4 words (one 32-byte
 // sector per row) in shared memory; each warp transposes 64 x 64 blocks with
-// four warp-wide 32 x 32 butterflies (transpose32) into a shared output tile
+// four warp-wide 32 x 32 butterflies (transpose32m) into a shared output tile
 // (256 rows x 8 words), written back as 16-byte stores, 64 contiguous bytes
 // per output row. The kernel is bound by the L1/shared data pipe (ncu: 87 %,
 // 21 M shuffle + 27 M shared wavefronts at 65536^2, 10.6 M of them bank
