@@ -3,7 +3,7 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W]
                     [--impl b200|reference|stub] [--workload cfg3|cfg5]
-                    [--extra cfg5|none]
+                    [--extra cfg5|none] [--grid rows|PRxPC|auto]
 
 One JSON line on rank 0.
 
@@ -23,7 +23,9 @@ torch.distributed.run (one process per GPU, NCCL, NCCL_DEBUG=INFO on stderr)
 and exits non-zero if fewer than N CUDA devices are visible -- it never
 measures fewer GPUs than it reports. N > 1: C and A row-sharded and generated
 in place, B generated on rank 0 and broadcast over NVLink (NCCL) in K-panels
-inside the timed step; time = max over ranks.
+inside the timed step; time = max over ranks. `--grid PRxPC|auto` lays the N
+ranks out as a process grid instead (rank (i, j) owns C[rows_i, cols_j]; B's
+column block j is cut on grid row 0 and broadcast inside column group j).
 
 `--impl reference` times the reference algorithm's CPU port
 (oracle/libgf2oracle.so, a C restatement of gf2mat's M4RM + Strassen-
