@@ -57,3 +57,28 @@ def test_bench_process_grid_share_one_gpu():
     assert d["n_gpus"] == 4 and d["verified_sha256"] is True
     assert d["e2e"]["verified_vs_device_result"] is True
     assert d["config"]["parallelism"].startswith("grid2x2")
+
+
+@pytest.mark.parametrize("nproc,grid", [(2, "rows"), (4, "2x2")])
+def test_example_sharded_mul_on_one_gpu(nproc, grid):
+    """examples/sharded_mul.py under torchrun, all ranks on cuda:0 over gloo:
+    the row-sharded layout and a 2 x 2 process grid, every block
+    Freivalds-checked against the full B."""
+    import socket
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k, None)
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={port}",
+                          os.path.join(ROOT, "examples", "sharded_mul.py"), "--size", "6144", "--grid", grid,
+                          "--npanels", "3", "--backend", "gloo", "--one-gpu"],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, (out.stdout + out.stderr)[-3000:]
+    assert "Freivalds on every block: True" in out.stdout
