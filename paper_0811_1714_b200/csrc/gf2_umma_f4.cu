@@ -31,15 +31,6 @@ constexpr int F4_EPI_BYTES = 4 * 32 * 4 * 8;  // 4 warps x 32 rows x 4 words
 constexpr int F4_SMEM = F4_STG * (F4_A_ST + F4_B_ST) + 1024 + F4_EPI_OFF + F4_EPI_BYTES;
 constexpr int F4_SF_COL = 2 * F4_BN;       // TMEM columns 448..511: constant scale factors
 constexpr int64_t F4_KCHUNK = 8192;
-// Option (off): accumulators start at 2^23 instead of 0 (the epilogue
-// re-biases the columns it has read before handing the buffer back; every
-// MMA accumulates), so the f32 sum 2^23 + S holds S in its mantissa and bit 0
-// is the parity with no add in the epilogue. Bit-exact on every test (the
-// MMA accumulates exactly at 2^23), but the re-bias stores and their
-// tcgen05.wait::st sit on the accumulator hand-back: cfg2 at cutoff 1024
-// 31.5 -> 36.2 us, cfg3 unchanged (0.899 vs 0.900 ms). Measured, kept off.
-constexpr bool F4_BIAS_ACC = false;
-constexpr uint32_t F4_BIAS = 0x4B000000u;  // 2^23
 static_assert(F4_SMEM <= 232448, "k_umma_f4 shared memory");
 
 // word t of a K-vector's 32 nibble bytes (see the permutation above)
@@ -268,20 +259,13 @@ __device__ __forceinline__ void tmem_fill32(uint32_t taddr, uint32_t val) {
 // gathered into one word with two-level byte permutes (3 PRMT); the 8 words
 // k = 0..7 then go to bit 7 - k of every byte with one shift and one masked
 // OR each: 56 instructions per 32 columns instead of 96.
-template <bool BIASED>
 __device__ __forceinline__ uint32_t parity_pack32(const uint32_t *v) {
     uint32_t u[32];
 #pragma unroll
-    for (int j = 0; j < 32; j += 2) {
-        if (BIASED) {  // accumulator already holds 2^23 + S
-            u[j] = v[j];
-            u[j + 1] = v[j + 1];
-        } else {
-            asm("{\n.reg .b64 a, r;\nmov.b64 a, {%2, %3};\nadd.rn.f32x2 r, a, %4;\nmov.b64 {%0, %1}, r;\n}\n"
-                : "=r"(u[j]), "=r"(u[j + 1])
-                : "r"(v[j]), "r"(v[j + 1]), "l"(0x4B0000004B000000ULL));
-        }
-    }
+    for (int j = 0; j < 32; j += 2)
+        asm("{\n.reg .b64 a, r;\nmov.b64 a, {%2, %3};\nadd.rn.f32x2 r, a, %4;\nmov.b64 {%0, %1}, r;\n}\n"
+            : "=r"(u[j]), "=r"(u[j + 1])
+            : "r"(v[j]), "r"(v[j + 1]), "l"(0x4B0000004B000000ULL));
     uint32_t pk = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -423,9 +407,6 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
         const uint32_t lanes = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
 #pragma unroll
         for (int h = 0; h < 2; ++h) tmem_fill32(lanes + F4_SF_COL + 32 * h, 0x7F7F7F7Fu);
-        if (F4_BIAS_ACC)  // both accumulators start at 2^23
-#pragma unroll
-            for (int c = 0; c < 2 * F4_BN / 32; ++c) tmem_fill32(lanes + 32 * c, F4_BIAS);
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
     }
     tc_fence_before();
@@ -516,7 +497,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
 #pragma unroll
                     for (int k = 0; k < BK / 32; ++k)
                         umma_f4(taddr, ad + 2 * k, bd + 2 * k, idesc,
-                                (F4_BIAS_ACC || kb > kb0 || k > 0) ? 1u : 0u, sfa, sfb);
+                                (kb > kb0 || k > 0) ? 1u : 0u, sfa, sfb);
                     umma_commit_cg<2>(bar_empty + 8 * stage);
                 }
                 __syncwarp();
@@ -559,15 +540,9 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1)
                 packed[c] = 0;
                 if (c < nch) {
                     if (c + 1 < nch) TMEM_LD32(trow + (c + 1) * 32, vb[(c + 1) & 1]);
-                    packed[c] = parity_pack32<F4_BIAS_ACC>(vb[c & 1]);
+                    packed[c] = parity_pack32(vb[c & 1]);
                     if (c + 1 < nch) TMEM_WAIT_LD32(vb[(c + 1) & 1]);
                 }
-            }
-            if (F4_BIAS_ACC) {  // re-bias the columns this tile used
-#pragma unroll
-                for (int c = 0; c < F4_BN / 32; ++c)
-                    if (c < nch) tmem_fill32(trow + c * 32, F4_BIAS);
-                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
             }
             tc_fence_before();
             mbar_arrive_leader(bar_tempty + 8 * acc);
